@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""bench.py — KV load throughput of libstrata on B200 (BASELINE.json metric).
+
+One "step" = one strata_load of the whole cached prefix, every layer (all §8(a) rows: planning,
+index fetch + layout transform, host->HBM movement, per-layer events) — for the default workload
+BASELINE.json configs[1]: Llama-3.1-8B geometry (32 layers, 8 KV heads, d=128, bf16), a 32K-token
+prefix, page size 1, randomly fragmented pages, 4 GiB per step (> 126 MB L2, so no flush needed).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl strata|reference] [--config ...] [--page-size P]
+
+Multi-GPU (torchrun): every rank loads its own replica workload over its own PCIe link (weak
+scaling, no data-path collective; NCCL only for the start barrier and the max-over-ranks timing).
+Rank 0 prints ONE JSON line.  ``--impl reference`` times the CPU oracle (oracle/, test
+infrastructure) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import kvgen  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="strata", choices=["strata", "reference"])
+    ap.add_argument("--config", default="llama8b_32k", choices=list(kvgen.CONFIGS))
+    ap.add_argument("--page-size", type=int, default=None)
+    ap.add_argument("--engine", type=int, default=0, help="0 default, 1 LDG, 2 TMA")
+    ap.add_argument("--num-ctas", type=int, default=0)
+    ap.add_argument("--frag", default="perm", choices=["perm", "churn"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args, rank: int, world: int):
+    """Per-rank geometry + request tables (replicas of the config; the TP config is already the
+    per-rank head slice)."""
+    g = kvgen.geometry(args.config, P=args.page_size)
+    n = kvgen.CONFIGS[args.config]["n"]
+    rng = kvgen.rng_for(args.seed * 1000 + rank)
+    if args.frag == "perm":
+        q = kvgen.make_requests(rng, n, g.P, g.C, g.num_pages, g.num_chunks)
+    else:
+        q = kvgen.make_requests(rng, n, g.P, g.C, g.num_pages, g.num_chunks, frag="churn")
+    return g, q
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 12.0):
+    """The oracle as it stands (oracle/oracle.c, OpenMP over all host cores), timed on this box on the
+    same workload: DRAM->DRAM into host images of the device pool (SURVEY.md §8d "Oracle timing")."""
+    import oracle
+    oracle.build()
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [np.empty(nb, np.uint8) for _ in range(g.L)]
+    v = [np.empty(nb, np.uint8) for _ in range(g.L)]
+    for a in k + v:
+        a.fill(0)   # fault the pages in outside the timed region
+    threads = oracle.max_threads()
+    bytes_per = 2 * g.L * q.total_tokens * g.token_bytes
+    times = []
+    t_start = time.time()
+    while not times or (time.time() - t_start < budget_s and len(times) < 5):
+        t0 = time.perf_counter()
+        oracle.load(g, host, k, v, q, 0, g.L, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    best = statistics.median(times)
+    return {"value": round(bytes_per / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": f"full {q.total_tokens}-token {g.L}-layer load of the bench workload, "
+                      f"{len(times)} reps, median; DRAM->DRAM, {threads} OpenMP threads",
+            "ms_per_load": round(best * 1e3, 2)}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    g, q = workload(args, 0, 1)
+    import oracle
+    oracle.build()
+    host = np.empty(g.host_bytes, np.uint8)
+    kvgen.fill_random(host, args.seed)
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [np.zeros(nb, np.uint8) for _ in range(g.L)]
+    v = [np.zeros(nb, np.uint8) for _ in range(g.L)]
+    threads = oracle.max_threads()
+    bytes_per = 2 * g.L * q.total_tokens * g.token_bytes
+    for _ in range(args.warmup):
+        oracle.load(g, host, k, v, q, 0, g.L, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.load(g, host, k, v, q, 0, g.L, nthreads=threads)
+    dt = time.perf_counter() - t0
+    value = bytes_per * args.steps / dt / 1e9
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic", "config": _config(args, g, q),
+            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "oracle",
+                             "sample": f"full workload per step ({q.total_tokens} tokens x {g.L} layers), "
+                                       f"DRAM->DRAM on the host cores"},
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(args, g, q):
+    return {"workload": args.config, "layers": g.L, "kv_heads_per_gpu": g.H, "head_dim": g.D, "kv_dtype": "bf16",
+            "page_size": g.P, "host_chunk_tokens": g.C, "tokens_per_gpu": q.total_tokens,
+            "requests": q.R, "fragmentation": args.frag, "bytes_per_step_per_gpu": 2 * g.L * q.total_tokens * g.token_bytes,
+            "l2": "no flush: each step moves 4+ GiB, far above the 126 MB L2", "parallelism": f"replicas x{args.gpus}"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_18572_b200 as st
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    g, q = workload(args, rank, world)
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks, device=local)
+    kvgen.fill_random(pool.host, args.seed * 1000 + rank)
+    reqs = st.Requests.from_kvgen(q, device=local)
+    bytes_step = 2 * g.L * q.total_tokens * g.token_bytes
+    io = torch.cuda.Stream()
+
+    def step():
+        return pool.load(reqs, 0, g.L, stream=io, engine=args.engine, num_ctas=args.num_ctas)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(io)
+        last = None
+        for _ in range(args.steps):
+            last = step()
+        end.record(io)
+        barrier()
+    elapsed = start.elapsed_time(end) / 1e3
+    # per-layer (= per-launch) durations of the last timed step, from the library's own events
+    t_layer = [pool.layer_elapsed_ms(last, l) for l in range(g.L)]
+    launch_ms = [t_layer[0]] + [b - a for a, b in zip(t_layer, t_layer[1:])]
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_max = float(t.item())
+    value = bytes_step * world * args.steps / elapsed_max / 1e9
+
+    # link roofline: one contiguous cudaMemcpyAsync of the same bytes-per-layer from the same host tier
+    scratch = torch.empty(bytes_step // g.L, dtype=torch.uint8, device="cuda")
+    rt = []
+    for i in range(13):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(io)
+        for _l in range(4):
+            st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, scratch.numel(), io)
+        b.record(io)
+        b.synchronize()
+        if i >= 3:
+            rt.append(4 * scratch.numel() / (a.elapsed_time(b) / 1e3) / 1e9)
+    link_peak = statistics.median(rt)
+    del scratch
+
+    # e2e through the public API with host buffers: upload the step's tables from pinned host
+    # memory, load (the KV itself crosses host->device inside), read back the last loaded row.
+    hc_pin = torch.from_numpy(reqs.host_chunks_h).pin_memory()
+    dp_pin = torch.from_numpy(reqs.dev_pages_h).pin_memory()
+    sentinel = torch.empty(16, dtype=torch.uint8).pin_memory()
+    last_page = int(q.dev_pages[-1])
+    e2e_steps = max(3, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        with torch.cuda.stream(io):
+            reqs.host_chunks_d.copy_(hc_pin, non_blocking=True)
+            reqs.dev_pages_d.copy_(dp_pin, non_blocking=True)
+        step()
+        with torch.cuda.stream(io):
+            sentinel.copy_(v[g.L - 1][last_page * g.P * g.token_bytes: last_page * g.P * g.token_bytes + 16],
+                           non_blocking=True)
+        io.synchronize()
+    e2e_dt = time.perf_counter() - t0
+    te = torch.tensor([e2e_dt], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = bytes_step * world * e2e_steps / float(te.item()) / 1e9
+    h2d = bytes_step + 4 * (reqs.host_chunks_h.size + reqs.dev_pages_h.size)
+
+    out = None
+    if rank == 0:
+        per_launch_bytes = bytes_step // g.L
+        avg_launch = statistics.mean(launch_ms[1:]) if len(launch_ms) > 1 else launch_ms[0]
+        achieved = per_launch_bytes / (avg_launch / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(f"{args.config}_P{g.P}")
+        peaks = {}
+        mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(mp):
+            peaks = json.load(open(mp))
+        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(g, q, pool.host)
+        batches = -(-q.R // 128)
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(elapsed_max / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": _config(args, g, q),
+            "ms_per_32k_load": round(elapsed_max / args.steps * 1e3 * 32768 / q.total_tokens, 3),
+            "frac_of_link": round(value / world / link_peak, 4),
+            "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3), "peak": round(link_peak, 3),
+                         "unit": "GB/s", "frac": round(achieved / link_peak, 4), "traffic": traffic,
+                         "kernel": "strata load kernel (one launch per layer)",
+                         "per_launch_bytes": per_launch_bytes, "avg_launch_ms": round(avg_launch, 4),
+                         "peak_source": "contiguous pinned cudaMemcpyAsync H2D from the same registered host "
+                                        "tier, measured in this run (PCIe Gen5 x16 nominal 64 GB/s)",
+                         "hbm": {"achieved": round(achieved, 3), "peak": hbm_peak,
+                                 "frac": round(achieved / hbm_peak, 5),
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": 16},
+            "gpu_launches": args.steps * g.L * batches,
+            "clocks": clocks.summary(),
+            "engine": args.engine, "num_ctas": args.num_ctas,
+        }
+        print(json.dumps(out), flush=True)
+    pool.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,181 @@
+/*
+ * strata.h — C ABI of libstrata, the B200-native GPU-assisted KV-cache I/O path of
+ * "Strata: Hierarchical Context Caching for Long Context Language Model Serving" (arXiv 2508.18572).
+ *
+ * The library moves cached KV between a pinned, GPU-mapped host tier and the GPU's paged KV pool:
+ *
+ *   strata_load     host tier -> device pool   page-table-indexed gather + layout transform
+ *   strata_offload  device pool -> host tier   the matching scatter ("backup")
+ *
+ * Both are sm_100a kernels that read/write host memory through zero-copy UVA mappings instead of
+ * one cudaMemcpyAsync per page ("GPU-assisted I/O": a kernel with thousands of threads, each moving
+ * a small chunk through registers or shared memory, §4.2), and both record one
+ * CUDA event per layer so a consumer can start layer l while later layers still stream in
+ * (PAPER.md:227 §4.1, :281 §4.2.1).
+ *
+ * LAYOUTS (DESIGN.md §3 readings R1-R5)
+ *   Host tier, page-first ("arranges layers of a page contiguously"):
+ *     num_chunks chunks of C tokens; chunk = [L][K,V][C][H][D] elements of e bytes,
+ *     chunk_bytes = L*2*C*H*D*e.  Token ho of chunk hc, layer l, kv, head h starts at
+ *       host_base + hc*chunk_bytes + ((l*2 + kv)*C + ho)*H*D*e + h*D*e.
+ *   Device pool, layer-first, paged: one K and one V buffer per layer,
+ *     caller-owned; token slot (page pg, offset po < P), head h starts at
+ *       {k,v}_ptrs[l] + pg*page_stride + po*token_stride + h*head_stride.
+ *     Default strides (0) are NHD: token_stride = H*D*e, head_stride = D*e, page_stride = P*H*D*e.
+ *   Request r moves num_tokens[r] tokens; token i (0-based in this call) lives at
+ *       host:   ci = chunk_offset[r] + i, chunk host_chunks[chunk_start[r] + ci / C], position ci % C
+ *       device: pi = page_offset[r]  + i, page  dev_pages [page_start[r]  + pi / P], offset   pi % P
+ *
+ * DATA IS OPAQUE BYTES: no conversion, no rounding; NaN payloads and -0.0 survive (R9).
+ *
+ * ERRORS: every call returns int, STRATA_OK (0) on success, a negative STRATA_ERR_* otherwise;
+ * strata_last_error() gives a thread-local message for the last failure.  No C++ exception crosses
+ * the ABI.  Argument, alignment and range checks of host-side values are synchronous.  Index-range
+ * and duplicate-destination checks of the device index lists run only when the pool has
+ * STRATA_VALIDATE (or env STRATA_VALIDATE=1): a device check kernel plus a stream synchronisation.
+ * Asynchronous kernel faults surface as STRATA_ERR_CUDA on a later call.
+ *
+ * THREADING: a pool handle is single-writer (one thread at a time); distinct handles are
+ * independent.
+ */
+#ifndef STRATA_H
+#define STRATA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same types as cudaStream_t / cudaEvent_t (CUDA runtime), declared here so consumers of this
+ * header need no CUDA headers. */
+struct CUstream_st;
+struct CUevent_st;
+typedef struct CUstream_st* strata_stream_t;
+typedef struct CUevent_st* strata_event_t;
+
+typedef struct strata_pool* strata_pool_t; /* opaque, library-owned */
+
+enum strata_status {
+  STRATA_OK = 0,
+  STRATA_ERR_INVALID_ARG = -1,  /* null pointer, bad size or range in a host-side value */
+  STRATA_ERR_ALIGNMENT = -2,    /* base/stride not a multiple of 16, or H*D*e % 16 != 0 (R12) */
+  STRATA_ERR_INDEX_RANGE = -3,  /* (validate) chunk/page index outside the pool or list */
+  STRATA_ERR_DUPLICATE = -4,    /* (validate) two tokens of one call target the same destination */
+  STRATA_ERR_CUDA = -5,         /* a CUDA runtime call failed (incl. an earlier async fault) */
+  STRATA_ERR_OOM = -6,          /* host allocation / registration failed */
+  STRATA_ERR_UNSUPPORTED = -7,  /* feature not available on this device / build */
+  STRATA_ERR_STALE_TICKET = -8  /* ticket older than the event ring, or not issued yet */
+};
+
+enum strata_pool_flags {
+  STRATA_HOST_HUGEPAGES = 1,     /* library-allocated host tier: MAP_HUGETLB, else THP madvise */
+  STRATA_HOST_WRITECOMBINED = 2, /* library-allocated host tier via cudaHostAllocWriteCombined */
+  STRATA_VALIDATE = 4,           /* check index lists on the device before every transfer */
+  STRATA_HOST_NO_NUMA_BIND = 8   /* do not bind library-allocated host memory to the GPU's node */
+};
+
+/* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
+enum strata_engine {
+  STRATA_ENGINE_DEFAULT = 0, /* library choice (currently STRATA_ENGINE_TMA) */
+  STRATA_ENGINE_LDG = 1,     /* warps, 16-byte LDG/STG register staging, warp index broadcast */
+  STRATA_ENGINE_TMA = 2      /* one warp per CTA, cp.async.bulk through a shared-memory ring */
+};
+
+typedef struct {
+  int32_t device;                 /* CUDA device ordinal the pool lives on */
+  int32_t num_layers;             /* L >= 1 */
+  int32_t num_heads;              /* H >= 1: this GPU's KV-head slice (TP shard) */
+  int32_t head_dim;               /* D >= 1 */
+  int32_t elem_bytes;             /* e >= 1 (2 for fp16/bf16) */
+  int32_t page_size;              /* P >= 1: device tokens per page */
+  int32_t chunk_tokens;           /* C >= 1: host tokens per chunk */
+  int32_t flags;                  /* strata_pool_flags */
+  void* const* k_ptrs;            /* [num_layers] device base of each layer's K buffer (copied) */
+  void* const* v_ptrs;            /* [num_layers] device base of each layer's V buffer (copied) */
+  int64_t page_stride;            /* device bytes between pages   (0 = P*H*D*e) */
+  int64_t token_stride;           /* device bytes between tokens  (0 = H*D*e) */
+  int64_t head_stride;            /* device bytes between heads   (0 = D*e) */
+  int64_t num_pages;              /* device capacity in pages (>= 1) */
+  void* host_base;                /* caller host memory to register, or NULL: library allocates */
+  int64_t num_chunks;             /* host capacity in chunks (>= 1) */
+} strata_pool_desc;
+
+typedef struct {
+  int32_t num_reqs;               /* R >= 0 */
+  int32_t layer_begin;            /* l0, half-open layer range [l0, l1) (R11) */
+  int32_t layer_end;              /* l1, 0 <= l0 <= l1 <= L */
+  int32_t engine;                 /* strata_engine */
+  int32_t num_ctas;               /* SM quota; 0 = library default */
+  int32_t threads;                /* threads per CTA for STRATA_ENGINE_LDG; 0 = default */
+  const int64_t* num_tokens;      /* [R] host: tokens to move per request (>= 0) */
+  const int32_t* host_chunks;     /* device int32: all requests' chunk lists concatenated */
+  const int64_t* chunk_start;     /* [R] host: start of request r's list in host_chunks */
+  const int32_t* dev_pages;       /* device int32: all requests' page lists concatenated */
+  const int64_t* page_start;      /* [R] host: start of request r's list in dev_pages */
+  const int32_t* chunk_offset;    /* [R] host or NULL (= 0): token offset inside the first chunk */
+  const int32_t* page_offset;     /* [R] host or NULL (= 0): token offset inside the first page */
+  int64_t host_chunks_len;        /* entries in host_chunks (0 = unknown: list bounds unchecked) */
+  int64_t dev_pages_len;          /* entries in dev_pages   (0 = unknown) */
+} strata_xfer;
+
+/* Register the host tier and bind it to the device pool described by *d.
+ * Host memory: if d->host_base != NULL it must hold num_chunks*chunk_bytes bytes, 16-byte aligned;
+ * the library page-locks and maps it (cudaHostRegisterMapped|Portable) and unregisters it in
+ * strata_unregister_host_pool; the caller keeps ownership.  If NULL, the library allocates it
+ * (NUMA-local to the GPU, pre-touched, optionally huge pages / write-combined), owns and frees it.
+ * Device buffers stay caller-owned and must outlive the handle.
+ * Errors: INVALID_ARG, ALIGNMENT, OOM, CUDA.  On error *out is set to NULL. */
+int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out);
+
+/* Wait for the pool's outstanding operations, unregister (and free if library-owned) the host
+ * tier, destroy the events.  NULL is a no-op. */
+int strata_unregister_host_pool(strata_pool_t p);
+
+/* Host address and size of the registered host tier (for filling / reading it on the CPU). */
+int strata_host_pool_ptr(strata_pool_t p, void** host_base, size_t* bytes);
+
+/* LOAD: for every request r, token i < num_tokens[r], layer l in [l0,l1), kv, head: copy D*e bytes
+ * from the host tier to the device pool (addresses in the LAYOUTS block).  Enqueued on `stream`;
+ * layers are processed in increasing order and event (ticket, l) completes once every byte of
+ * layer l of this call is in the device pool.  n = 0 or l0 = l1 is a successful no-op that still
+ * records the events of the covered layers.  Index lists must stay valid until the stream passes
+ * the operation (same contract as cudaMemcpyAsync).  Duplicate destinations are a caller error
+ * (rejected under STRATA_VALIDATE, unspecified otherwise); duplicate sources are legal.
+ * *ticket (nullable) receives the operation's ticket for strata_layer_event. */
+int strata_load(strata_pool_t p, const strata_xfer* x, strata_stream_t stream, uint64_t* ticket);
+
+/* OFFLOAD ("backup"): the inverse scatter, device pool -> host tier, same
+ * arguments and event semantics.  Host bytes are CPU-visible once the layer's event (or the
+ * stream) has completed. */
+int strata_offload(strata_pool_t p, const strata_xfer* x, strata_stream_t stream, uint64_t* ticket);
+
+/* Per-layer completion (§4.1): the library-owned event recorded after layer `layer`
+ * of operation `ticket` (0 = the latest operation).  The event stays valid until the ring slot is
+ * reused 8 operations later; an older ticket returns STRATA_ERR_STALE_TICKET.  A layer outside the
+ * operation's range returns STRATA_ERR_INVALID_ARG.  Use with cudaStreamWaitEvent /
+ * cudaEventSynchronize; never destroy it. */
+int strata_layer_event(strata_pool_t p, uint64_t ticket, int32_t layer, strata_event_t* out);
+
+/* Consumer-side wait: make stream `consumer` wait until layer `layer` of operation
+ * `ticket` (0 = latest) is complete — cudaStreamWaitEvent on the layer's event.  Errors as
+ * strata_layer_event, plus STRATA_ERR_CUDA. */
+int strata_wait_layer(strata_pool_t p, uint64_t ticket, int32_t layer, strata_stream_t consumer);
+
+/* Milliseconds from the start of operation `ticket` (0 = latest) on its stream to the completion of
+ * layer `layer` (CUDA event timing).  Blocks until that layer is complete.  Errors as
+ * strata_layer_event, plus STRATA_ERR_CUDA. */
+int strata_layer_elapsed_ms(strata_pool_t p, uint64_t ticket, int32_t layer, float* ms);
+
+/* Thread-local message describing the last non-OK return on this thread ("" if none). */
+const char* strata_last_error(void);
+
+/* Library version as 10000*major + 100*minor + patch. */
+int strata_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STRATA_H */

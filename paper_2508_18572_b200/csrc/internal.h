@@ -1,0 +1,112 @@
+// internal.h — libstrata internals shared by the API layer (api.cpp, baselines.cpp) and the
+// sm_100a kernels (kernels.cu).  Not part of the ABI; see include/strata.h for the contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/strata.h"
+
+namespace strata {
+
+// Requests per kernel launch: their tables travel in the kernel parameters (no staging copy, so a
+// call is graph-capturable).  Calls with more requests are split into several launches per layer.
+constexpr int kMaxReqsPerLaunch = 128;
+constexpr int kEventRing = 8;          // operations whose per-layer events stay valid
+
+// Per-launch request table (struct of arrays).  Flat token index g in [0, ntok) enumerates the
+// tokens of the launch's requests in order; request r owns [tok_end[r-1], tok_end[r]).
+struct ReqTable {
+  int32_t n;
+  int32_t tok_end[kMaxReqsPerLaunch];
+  int32_t chunk_base[kMaxReqsPerLaunch];   // chunk_start[r]: first entry of r's chunk list
+  int32_t page_base[kMaxReqsPerLaunch];    // page_start[r]
+  int32_t off_c[kMaxReqsPerLaunch];        // token offset inside the first host chunk
+  int32_t off_p[kMaxReqsPerLaunch];        // token offset inside the first device page
+};
+
+// Everything one per-layer launch needs; passed by value as a __grid_constant__ parameter.
+struct XferParams {
+  // geometry (bytes unless noted)
+  int32_t C, P;                 // host chunk tokens, device page tokens
+  int32_t H;                    // heads of this GPU's slice
+  int32_t tok_bytes;            // S_tok = H*D*e (one token, one of K/V, one layer)
+  int32_t head_bytes;           // D*e
+  int32_t vpt;                  // 16-byte vectors per token row = tok_bytes/16
+  int32_t vpt_shift;            // log2(vpt) if vpt is a power of two, else -1
+  int32_t vph;                  // 16-byte vectors per head = head_bytes/16
+  int32_t rows_per_group;       // LDG engine: token rows handled by one warp iteration (<= 32)
+  int32_t tma_rows;             // TMA engine: token rows per pipeline stage (<= 32)
+  int32_t tma_stages;           // TMA engine: pipeline depth
+  int32_t tma_stage_bytes;      // TMA engine: bytes per stage (>= tma_rows * tok_bytes)
+  int64_t chunk_bytes;          // L*2*C*S_tok
+  int64_t layer_off;            // byte offset of (layer, K) inside a host chunk: l*2*C*S_tok
+  int64_t kv_off;               // byte offset from K to V inside a chunk layer: C*S_tok
+  int64_t page_stride, token_stride, head_stride;
+  // data
+  char* host;                   // device-visible address of the host tier (UVA)
+  char* kbase;                  // this layer's K buffer
+  char* vbase;                  // this layer's V buffer
+  const int32_t* host_chunks;   // device index lists
+  const int32_t* dev_pages;
+  int32_t ntok;                 // tokens in this launch
+  int32_t pad_;
+  ReqTable rt;
+};
+
+struct ValidateParams {
+  int32_t C, P;
+  int32_t ntok;
+  int32_t dir;                  // 0 load (destinations = device slots), 1 offload (host slots)
+  int64_t num_pages, num_chunks;
+  int64_t chunks_len, pages_len;   // list lengths (0 = unknown)
+  const int32_t* host_chunks;
+  const int32_t* dev_pages;
+  uint32_t* bitmap;             // one bit per destination slot, zeroed by the caller
+  int32_t* err;                 // bit 0: index range, bit 1: duplicate
+  ReqTable rt;
+};
+
+// Kernel launchers (kernels.cu).  dir: 0 = load (host -> device), 1 = offload (device -> host).
+cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s);
+cudaError_t launch_tma(const XferParams& p, int dir, int ctas, cudaStream_t s);
+cudaError_t launch_validate(const ValidateParams& v, cudaStream_t s);
+// Largest dynamic shared memory the TMA engine may use per CTA on this device.
+int tma_smem_limit();
+// Shared-memory bytes in front of the TMA ring (mbarriers + per-stage address tables).
+int tma_header_bytes(int stages);
+// Opt the TMA kernels in to `smem` bytes of dynamic shared memory on the current device.
+cudaError_t tma_prepare(int smem);
+constexpr int kTmaMaxStages = 32;
+
+// Records `msg` as this thread's strata_last_error() and returns `code` (api.cpp).
+int set_last_error(int code, const char* msg);
+
+}  // namespace strata
+
+struct strata_pool {
+  strata_pool_desc d;                 // copy; k_ptrs/v_ptrs re-pointed at the vectors below
+  std::vector<void*> k, v;
+  int64_t tok_bytes, head_bytes, chunk_bytes;
+  int64_t page_stride, token_stride, head_stride;
+  // host tier
+  char* host = nullptr;               // host address
+  char* host_dev = nullptr;           // device-visible address (UVA: usually == host)
+  size_t host_bytes = 0;
+  int host_kind = 0;                  // 0 caller memory, 1 mmap (library), 2 cudaHostAlloc (library)
+  bool registered_by_us = false;
+  size_t map_bytes = 0;               // mmap length
+  // per-layer completion events: ring of kEventRing operations x L layers
+  std::vector<cudaEvent_t> events;
+  struct Op { uint64_t ticket; int32_t l0, l1; };
+  Op ops[strata::kEventRing];
+  uint64_t next_ticket = 1;
+  // validate scratch (device)
+  uint32_t* bitmap = nullptr;
+  size_t bitmap_words = 0;
+  int32_t* err_dev = nullptr;
+  int32_t* err_host = nullptr;        // pinned
+  int tma_smem = 0;
+};

@@ -1,0 +1,372 @@
+// kernels.cu — sm_100a kernels of libstrata: the GPU-assisted KV load (host tier -> paged device
+// pool) and offload (the inverse scatter), plus the STRATA_VALIDATE index checker.
+//
+// "instead of invoking standard cudaMemcpyAsync API repetitively with small data transfers, a
+//  GPU-assisted I/O job operates by launching a CUDA kernel ... Each thread is responsible for
+//  loading a small chunk of data from a source (either GPU global memory or CPU registered pinned
+//  memory) into its local register files and then streaming this data to a destination"
+//                                                           (§4.2)
+// The layout transform (page-first host chunk <-> layer-first paged pool) is address arithmetic on
+// each token row (§4.2.1) — row_addr() below.
+//
+// Two engines, bit-identical, chosen per call (strata_xfer.engine):
+//   LDG  warps own groups of token rows; lanes compute the row addresses (index fetch) and
+//        broadcast them with __shfl_sync; each lane keeps U independent 16-byte loads in flight
+//        (LDG.E.128 from the mapped host VA), then stores them.  Register staging as in the paper.
+//   TMA  one warp per CTA runs an S-stage shared-memory ring: host runs that are contiguous
+//        (consecutive tokens of one chunk) arrive with ONE cp.async.bulk each (UBLKCP), token rows
+//        leave with one bulk store each.  ~160-190 KB in flight per SM from a single warp, so the
+//        link saturates from very few SMs with almost no register / issue footprint (the paper's
+//        SM-quota goal).
+// Both are bound by the host link (PCIe Gen5 x16, measured 55.5 GB/s memcpy, 51.4 GB/s SM
+// zero-copy ceiling on the B200 box — profiles/r01/probe.jsonl); HBM sees < 1 % of its bandwidth.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace strata {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------------------------
+// Index fetch + layout transform for one token row.  Row = (kv, g): kv-major over the launch's
+// flat tokens (rows [0,N) are K, [N,2N) are V), so consecutive rows of one chunk are consecutive
+// host bytes.  Returns the host address and the device address of the row's first byte.
+__device__ __forceinline__ int find_req(const ReqTable& rt, int32_t g) {
+  int lo = 0, hi = rt.n - 1;  // first r with tok_end[r] > g
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (rt.tok_end[mid] > g) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void row_addr(const XferParams& p, int64_t row, char*& hp, char*& dp) {
+  const int kv = row >= p.ntok;
+  const int32_t g = static_cast<int32_t>(row - (kv ? p.ntok : 0));
+  const int r = find_req(p.rt, g);
+  const int32_t i = g - (r ? p.rt.tok_end[r - 1] : 0);
+  const int32_t ci = p.rt.off_c[r] + i;         // position in the request's host chunk list
+  const int32_t pi = p.rt.off_p[r] + i;         // position in the request's device page list
+  const int32_t cq = ci / p.C, cr = ci - cq * p.C;
+  const int32_t pq = pi / p.P, pr = pi - pq * p.P;
+  const int64_t hc = __ldg(p.host_chunks + p.rt.chunk_base[r] + cq);
+  const int64_t pg = __ldg(p.dev_pages + p.rt.page_base[r] + pq);
+  // host: chunk hc, layer l, kv, token cr            (page-first)
+  hp = p.host + hc * p.chunk_bytes + p.layer_off + kv * p.kv_off + static_cast<int64_t>(cr) * p.tok_bytes;
+  // device: page pg, offset pr of this layer's K/V  (layer-first paged pool)
+  dp = (kv ? p.vbase : p.kbase) + pg * p.page_stride + static_cast<int64_t>(pr) * p.token_stride;
+}
+
+// ---------------------------------------------------------------------------------------------
+// 16-byte vector accesses.  Sources are read once: no L1 allocation.
+__device__ __forceinline__ int4 ld_stream(const void* ptr) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
+  return r;
+}
+__device__ __forceinline__ void st_vec(void* ptr, const int4& v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// LDG engine.  DIR 0: host -> device, DIR 1: device -> host.  CONTIG: device rows head-contiguous
+// (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
+template <int U, bool CONTIG, int DIR>
+__global__ void __launch_bounds__(1024) ldg_kernel(const __grid_constant__ XferParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t nrows = 2LL * p.ntok;
+  const int RG = p.rows_per_group;
+  const int64_t ngroups = (nrows + RG - 1) / RG;
+  for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+    const int64_t row0 = gi * RG;
+    const int nr = static_cast<int>(min(static_cast<int64_t>(RG), nrows - row0));
+    char* hp = nullptr;
+    char* dp = nullptr;
+    if (lane < nr) row_addr(p, row0 + lane, hp, dp);   // index fetch by lane, broadcast below
+    const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
+    const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
+    const int nvec = nr * p.vpt;
+    for (int base = 0; base < nvec; base += 32 * U) {
+      int4 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int idx = base + j * 32 + lane;
+        const int rl = p.vpt_shift >= 0 ? (idx >> p.vpt_shift) : (idx / p.vpt);
+        const int w = idx - rl * p.vpt;
+        const uint64_t s = __shfl_sync(kFull, my_src, rl & 31);
+        if (idx < nvec) {
+          const char* a;
+          if (DIR == 0 || CONTIG) {
+            a = reinterpret_cast<const char*>(s) + w * 16;
+          } else {
+            const int h = w / p.vph;
+            a = reinterpret_cast<const char*>(s) + h * p.head_stride + (w - h * p.vph) * 16;
+          }
+          v[j] = ld_stream(a);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int idx = base + j * 32 + lane;
+        const int rl = p.vpt_shift >= 0 ? (idx >> p.vpt_shift) : (idx / p.vpt);
+        const int w = idx - rl * p.vpt;
+        const uint64_t d = __shfl_sync(kFull, my_dst, rl & 31);
+        if (idx < nvec) {
+          char* a;
+          if (DIR == 1 || CONTIG) {
+            a = reinterpret_cast<char*>(d) + w * 16;
+          } else {
+            const int h = w / p.vph;
+            a = reinterpret_cast<char*>(d) + h * p.head_stride + (w - h * p.vph) * 16;
+          }
+          st_vec(a, v[j]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// TMA engine primitives (cp.async.bulk non-tensor copies + mbarrier transaction counts).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" :: "r"(smem_u32(b)), "r"(parity) : "memory");
+}
+// global (device or mapped host) -> shared, completes `bytes` on barrier `bar`
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// shared -> global (device or mapped host), tracked by this thread's bulk async-groups
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+constexpr int kTmaHeader = 8 * kTmaMaxStages;            // mbarriers
+
+__host__ __device__ constexpr int tma_table_bytes(int stages) { return stages * 32 * 12; }
+__host__ __device__ constexpr int tma_buf_offset(int stages) {
+  return (kTmaHeader + tma_table_bytes(stages) + 127) / 128 * 128;
+}
+
+// One warp per CTA.  Pieces of `tma_rows` consecutive token rows are distributed round-robin over
+// CTAs; piece k of this CTA uses stage k % S.
+template <int DIR, bool CONTIG>
+__global__ void __launch_bounds__(32, 1) tma_kernel(const __grid_constant__ XferParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.tma_stages;
+  const int T = p.tma_rows;
+  const int SB = p.tma_stage_bytes;
+  const int tok = p.tok_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* tab_addr = reinterpret_cast<uint64_t*>(smem + kTmaHeader);              // [S][32]
+  int32_t* tab_len = reinterpret_cast<int32_t*>(smem + kTmaHeader + S * 32 * 8);   // [S][32]
+  unsigned char* buf = smem + tma_buf_offset(S);
+  const int lane = threadIdx.x;
+
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  const int64_t nrows = 2LL * p.ntok;
+  const int64_t npieces = (nrows + T - 1) / T;
+  const int64_t my = npieces > blockIdx.x ? (npieces - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  auto issue = [&](int64_t k) {
+    const int s = static_cast<int>(k % S);
+    const int64_t row = (blockIdx.x + k * gridDim.x) * T + lane;
+    const bool valid = lane < T && row < nrows;
+    char* hp = nullptr;
+    char* dp = nullptr;
+    if (valid) row_addr(p, row, hp, dp);
+    // host-side runs: a lane starts a run unless its row directly follows the previous lane's
+    const uint64_t hprev = __shfl_up_sync(kFull, reinterpret_cast<uint64_t>(hp), 1);
+    const int vprev = __shfl_up_sync(kFull, static_cast<int>(valid), 1);
+    const bool head = valid && !(lane > 0 && vprev && hprev + tok == reinterpret_cast<uint64_t>(hp));
+    const unsigned heads = __ballot_sync(kFull, head);
+    const int nvalid = __popc(__ballot_sync(kFull, valid));
+    const unsigned later = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
+    const int run = (later ? __ffs(later) - 1 : nvalid) - lane;
+    unsigned char* st = buf + static_cast<size_t>(s) * SB;
+    if (DIR == 0) {
+      tab_addr[s * 32 + lane] = reinterpret_cast<uint64_t>(dp);
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nvalid * tok));
+      __syncwarp();
+      if (head) bulk_g2s(st + lane * tok, hp, static_cast<uint32_t>(run * tok), &full[s]);
+    } else {
+      tab_addr[s * 32 + lane] = reinterpret_cast<uint64_t>(hp);
+      tab_len[s * 32 + lane] = head ? run : 0;
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nvalid * tok));
+      __syncwarp();
+      if (valid) {
+        if (CONTIG) {
+          bulk_g2s(st + lane * tok, dp, static_cast<uint32_t>(tok), &full[s]);
+        } else {
+          for (int h = 0; h < p.H; ++h)
+            bulk_g2s(st + lane * tok + h * p.head_bytes, dp + h * p.head_stride,
+                     static_cast<uint32_t>(p.head_bytes), &full[s]);
+        }
+      }
+    }
+  };
+
+  auto consume = [&](int64_t k) {
+    const int s = static_cast<int>(k % S);
+    mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
+    unsigned char* st = buf + static_cast<size_t>(s) * SB;
+    if (DIR == 0) {
+      char* dp = reinterpret_cast<char*>(tab_addr[s * 32 + lane]);
+      if (dp) {
+        if (CONTIG) {
+          bulk_s2g(dp, st + lane * tok, static_cast<uint32_t>(tok));
+        } else {
+          for (int h = 0; h < p.H; ++h)
+            bulk_s2g(dp + h * p.head_stride, st + lane * tok + h * p.head_bytes,
+                     static_cast<uint32_t>(p.head_bytes));
+        }
+      }
+    } else {
+      const int run = tab_len[s * 32 + lane];
+      if (run) bulk_s2g(reinterpret_cast<char*>(tab_addr[s * 32 + lane]), st + lane * tok,
+                        static_cast<uint32_t>(run * tok));
+    }
+    bulk_commit();
+  };
+
+  const int64_t pro = my < S ? my : S;
+  for (int64_t k = 0; k < pro; ++k) issue(k);
+  for (int64_t k = 0; k < my; ++k) {
+    consume(k);
+    // refill the stage piece k-1 used once its stores have read shared memory
+    if (k >= 1 && k - 1 + S < my) {
+      bulk_wait_read1();
+      __syncwarp();
+      issue(k - 1 + S);
+    }
+  }
+  bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void validate_kernel(const __grid_constant__ ValidateParams v) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < v.ntok; g += stride) {
+    const int32_t gg = static_cast<int32_t>(g);
+    int lo = 0, hi = v.rt.n - 1;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (v.rt.tok_end[mid] > gg) hi = mid; else lo = mid + 1;
+    }
+    const int r = lo;
+    const int32_t i = gg - (r ? v.rt.tok_end[r - 1] : 0);
+    const int64_t ci = static_cast<int64_t>(v.rt.off_c[r]) + i;
+    const int64_t pi = static_cast<int64_t>(v.rt.off_p[r]) + i;
+    const int64_t cidx = v.rt.chunk_base[r] + ci / v.C;
+    const int64_t pidx = v.rt.page_base[r] + pi / v.P;
+    if ((v.chunks_len > 0 && cidx >= v.chunks_len) || (v.pages_len > 0 && pidx >= v.pages_len)) {
+      atomicOr(v.err, 1);
+      continue;
+    }
+    const int64_t hc = v.host_chunks[cidx];
+    const int64_t pg = v.dev_pages[pidx];
+    if (hc < 0 || hc >= v.num_chunks || pg < 0 || pg >= v.num_pages) {
+      atomicOr(v.err, 1);
+      continue;
+    }
+    const int64_t key = v.dir == 0 ? pg * v.P + pi % v.P : hc * v.C + ci % v.C;
+    const uint32_t bit = 1u << (key & 31);
+    const uint32_t old = atomicOr(v.bitmap + (key >> 5), bit);
+    if (old & bit) atomicOr(v.err, 2);
+  }
+}
+
+template <int U, bool CONTIG, int DIR>
+cudaError_t ldg_launch(const XferParams& p, int ctas, int threads, cudaStream_t s) {
+  ldg_kernel<U, CONTIG, DIR><<<ctas, threads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DIR, bool CONTIG>
+cudaError_t tma_launch(const XferParams& p, int ctas, cudaStream_t s) {
+  const int smem = tma_buf_offset(p.tma_stages) + p.tma_stages * p.tma_stage_bytes;
+  tma_kernel<DIR, CONTIG><<<ctas, 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s) {
+  const bool contig = p.head_stride == p.head_bytes;
+#define STRATA_LDG(U)                                                               \
+  if (unroll == U) {                                                                \
+    if (dir == 0) return contig ? ldg_launch<U, true, 0>(p, ctas, threads, s)       \
+                                : ldg_launch<U, false, 0>(p, ctas, threads, s);     \
+    return contig ? ldg_launch<U, true, 1>(p, ctas, threads, s)                     \
+                  : ldg_launch<U, false, 1>(p, ctas, threads, s);                   \
+  }
+  STRATA_LDG(4)
+  STRATA_LDG(8)
+#undef STRATA_LDG
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tma(const XferParams& p, int dir, int ctas, cudaStream_t s) {
+  const bool contig = p.head_stride == p.head_bytes;
+  if (dir == 0) return contig ? tma_launch<0, true>(p, ctas, s) : tma_launch<0, false>(p, ctas, s);
+  return contig ? tma_launch<1, true>(p, ctas, s) : tma_launch<1, false>(p, ctas, s);
+}
+
+cudaError_t launch_validate(const ValidateParams& v, cudaStream_t s) {
+  const int threads = 256;
+  int64_t blocks = (v.ntok + threads - 1) / threads;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 1184) blocks = 1184;
+  validate_kernel<<<static_cast<int>(blocks), threads, 0, s>>>(v);
+  return cudaGetLastError();
+}
+
+int tma_smem_limit() {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+  return optin;
+}
+
+int tma_header_bytes(int stages) { return tma_buf_offset(stages); }
+
+cudaError_t tma_prepare(int smem) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(tma_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(tma_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(tma_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  return cudaFuncSetAttribute(tma_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+}  // namespace strata

@@ -1,0 +1,108 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/*.h declares,
+and rejects bad arguments synchronously with the documented codes before touching CUDA."""
+import ctypes
+
+import pytest
+
+from paper_2508_18572_b200 import _lib
+from paper_2508_18572_b200._lib import PoolDesc, Xfer
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2508_18572_b200 import build
+    build.build()
+    return _lib.lib()
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _lib.declared_symbols()
+    assert len(names) >= 13, names
+    for n in names:
+        assert hasattr(lib, n), f"libstrata.so does not export {n}"
+    for n in ("strata_register_host_pool", "strata_load", "strata_offload", "strata_layer_event"):
+        assert n in names
+    assert lib.strata_version() >= 100
+
+
+def test_struct_layouts_match_header(lib):
+    # int32 x8 then pointers/int64 (see include/strata.h); 8-byte aligned, no padding surprises
+    assert ctypes.sizeof(PoolDesc) == 8 * 4 + 2 * 8 + 4 * 8 + 8 + 8
+    assert ctypes.sizeof(Xfer) == 6 * 4 + 7 * 8 + 2 * 8
+
+
+def _desc(**kw):
+    k = (ctypes.c_void_p * 2)(0x10000, 0x20000)
+    v = (ctypes.c_void_p * 2)(0x30000, 0x40000)
+    d = dict(device=0, num_layers=2, num_heads=2, head_dim=64, elem_bytes=2, page_size=16, chunk_tokens=64,
+             flags=0, k_ptrs=ctypes.cast(k, ctypes.POINTER(ctypes.c_void_p)),
+             v_ptrs=ctypes.cast(v, ctypes.POINTER(ctypes.c_void_p)), page_stride=0, token_stride=0,
+             head_stride=0, num_pages=256, host_base=None, num_chunks=64)
+    d.update(kw)
+    return PoolDesc(**d), (k, v)
+
+
+def _register(lib, desc):
+    h = ctypes.c_void_p()
+    rc = lib.strata_register_host_pool(ctypes.byref(desc), ctypes.byref(h))
+    return rc, h
+
+
+@pytest.mark.parametrize("field,value,code", [
+    ("num_layers", 0, _lib.STRATA_ERR_INVALID_ARG),
+    ("page_size", 0, _lib.STRATA_ERR_INVALID_ARG),
+    ("num_chunks", 0, _lib.STRATA_ERR_INVALID_ARG),
+    ("head_dim", 3, _lib.STRATA_ERR_ALIGNMENT),          # H*D*e = 12 bytes, not a multiple of 16 (R12)
+    ("token_stride", 8 + 256, _lib.STRATA_ERR_ALIGNMENT),
+    ("page_stride", 24, _lib.STRATA_ERR_ALIGNMENT),
+    ("host_base", 0x1008, _lib.STRATA_ERR_ALIGNMENT),
+    ("num_pages", 1 << 31, _lib.STRATA_ERR_INVALID_ARG),
+])
+def test_register_rejects_bad_descriptor(lib, field, value, code):
+    desc, keep = _desc(**{field: value})
+    rc, h = _register(lib, desc)
+    assert rc == code, lib.strata_last_error()
+    assert not h.value
+    assert lib.strata_last_error()
+
+
+def test_register_rejects_null_and_misaligned_layer_ptrs(lib):
+    assert lib.strata_register_host_pool(None, ctypes.byref(ctypes.c_void_p())) == _lib.STRATA_ERR_INVALID_ARG
+    k = (ctypes.c_void_p * 2)(0x10000, 0)
+    desc, keep = _desc(k_ptrs=ctypes.cast(k, ctypes.POINTER(ctypes.c_void_p)))
+    assert _register(lib, desc)[0] == _lib.STRATA_ERR_INVALID_ARG
+    k = (ctypes.c_void_p * 2)(0x10000, 0x10004)
+    desc, keep = _desc(k_ptrs=ctypes.cast(k, ctypes.POINTER(ctypes.c_void_p)))
+    assert _register(lib, desc)[0] == _lib.STRATA_ERR_ALIGNMENT
+
+
+def test_valid_descriptor_without_gpu_fails_in_cuda(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    desc, keep = _desc()
+    rc, h = _register(lib, desc)
+    assert rc == _lib.STRATA_ERR_CUDA
+    assert "cuda" in lib.strata_last_error().decode().lower()
+
+
+def test_null_pool_calls(lib):
+    x = Xfer()
+    assert lib.strata_load(None, ctypes.byref(x), None, None) == _lib.STRATA_ERR_INVALID_ARG
+    assert lib.strata_offload(None, ctypes.byref(x), None, None) == _lib.STRATA_ERR_INVALID_ARG
+    ev = ctypes.c_void_p()
+    assert lib.strata_layer_event(None, 0, 0, ctypes.byref(ev)) == _lib.STRATA_ERR_INVALID_ARG
+    assert lib.strata_unregister_host_pool(None) == _lib.STRATA_OK
+    assert lib.strata_host_pool_ptr(None, None, None) == _lib.STRATA_ERR_INVALID_ARG
+
+
+def test_product_has_no_oracle_dependency():
+    """The product package never imports the oracle (which is test infrastructure)."""
+    import os
+    import re
+    root = os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_2508_18572_b200")
+    for dirpath, _, files in os.walk(root):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"\boracle\b", re.sub(r"(#|//).*", "", text)), f

@@ -1,0 +1,91 @@
+"""N>1 host-side logic on CPU (gloo, world_size 2): KV-head sharding across ranks
+and the max-over-ranks timing reduction bench.py uses.  Each rank loads only its head slice from
+its own host tier; the gathered union must equal the full-head load."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import kvgen
+        import oracle
+        from kvgen import Geometry
+        oracle.build()
+        H_total = 8
+        full = Geometry(L=3, H=H_total, D=16, e=2, P=4, C=8, num_pages=64, num_chunks=16)
+        rng = kvgen.rng_for(42)      # identical tables on every rank (TP ranks share the mapping)
+        host_full = kvgen.random_bytes(rng, full.host_bytes)
+        q = kvgen.make_requests(rng, [37, 70], full.P, full.C, full.num_pages, full.num_chunks, offsets=True)
+        hs = kvgen.head_slice(rank, world, H_total)
+        g = Geometry(full.L, len(hs), full.D, full.e, full.P, full.C, full.num_pages, full.num_chunks)
+        # this rank's host tier holds only its heads (layout R1 with H_loc = H/T, R13)
+        host = np.ascontiguousarray(
+            host_full.reshape(full.num_chunks, full.L, 2, full.C, H_total, full.D * full.e)[:, :, :, :, hs.start:hs.stop]
+        ).reshape(-1)
+        nb = g.num_pages * g.P * g.token_bytes
+        k = [np.zeros(nb, np.uint8) for _ in range(g.L)]
+        v = [np.zeros(nb, np.uint8) for _ in range(g.L)]
+        oracle.load(g, host, k, v, q, 0, g.L)
+        mine = torch.from_numpy(np.stack(k + v))
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        # timing reduction: max over ranks
+        t = torch.tensor([1.0 + rank], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            nbf = full.num_pages * full.P * full.token_bytes
+            kf = [np.zeros(nbf, np.uint8) for _ in range(full.L)]
+            vf = [np.zeros(nbf, np.uint8) for _ in range(full.L)]
+            oracle.load(full, host_full, kf, vf, q, 0, full.L)
+            ok = True
+            hl = H_total // world
+            for i, img in enumerate(kf + vf):
+                cat = np.concatenate([p[i].numpy().reshape(-1, hl, full.D * full.e) for p in parts], axis=1)
+                ok &= np.array_equal(img.reshape(-1, H_total, full.D * full.e), cat)
+            out_q.put((bool(ok), float(t.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_head_sharded_union_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    ok, tmax = q.get(timeout=10)
+    assert ok, "union of head-slice loads differs from the full-head load"
+    assert tmax == float(world)
+
+
+def test_head_slice_partition():
+    import kvgen
+    for H, T in [(8, 1), (8, 2), (8, 4), (8, 8), (4, 2)]:
+        seen = []
+        for r in range(T):
+            seen += list(kvgen.head_slice(r, T, H))
+        assert seen == list(range(H))
+    with pytest.raises(ValueError):
+        kvgen.head_slice(0, 3, 8)
