@@ -229,14 +229,23 @@ def main():
         step()
     barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clocks:
         start.record(io)
         last = None
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            marks[i].record(io)
             last = step()
+        marks[-1].record(io)
         end.record(io)
         barrier()
     elapsed = start.elapsed_time(end) / 1e3
+    step_ms = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps))
+    step_stats = {"median_ms": round(statistics.median(step_ms), 3),
+                  "p10_ms": round(step_ms[int(0.1 * (len(step_ms) - 1))], 3),
+                  "p90_ms": round(step_ms[int(0.9 * (len(step_ms) - 1))], 3),
+                  "min_ms": round(step_ms[0], 3), "max_ms": round(step_ms[-1], 3),
+                  "cv": round(statistics.pstdev(step_ms) / statistics.mean(step_ms), 4)}
     # per-layer (= per-launch) durations of the last timed step, from the library's own events
     t_layer = [pool.layer_elapsed_ms(last, l) for l in range(g.L)]
     launch_ms = [t_layer[0]] + [b - a for a, b in zip(t_layer, t_layer[1:])]
@@ -310,6 +319,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": _config(args, g, q),
             "ms_per_32k_load": round(elapsed_max / args.steps * 1e3 * 32768 / q.total_tokens, 3),
+            "step_stats_rank0": step_stats,
             "frac_of_link": round(value / world / link_peak, 4),
             "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3), "peak": round(link_peak, 3),
                          "unit": "GB/s", "frac": round(achieved / link_peak, 4), "traffic": traffic,

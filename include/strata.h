@@ -73,14 +73,22 @@ enum strata_pool_flags {
   STRATA_HOST_HUGEPAGES = 1,     /* library-allocated host tier: MAP_HUGETLB, else THP madvise */
   STRATA_HOST_WRITECOMBINED = 2, /* library-allocated host tier via cudaHostAllocWriteCombined */
   STRATA_VALIDATE = 4,           /* check index lists on the device before every transfer */
-  STRATA_HOST_NO_NUMA_BIND = 8   /* do not bind library-allocated host memory to the GPU's node */
+  STRATA_HOST_NO_NUMA_BIND = 8,  /* do not bind library-allocated host memory to the GPU's node */
+  STRATA_HOST_CUDA_ALLOC = 16    /* library-allocated host tier via cudaHostAlloc(Mapped|Portable)
+                                    instead of mmap + cudaHostRegister */
 };
 
 /* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
 enum strata_engine {
-  STRATA_ENGINE_DEFAULT = 0, /* library choice (currently STRATA_ENGINE_TMA) */
-  STRATA_ENGINE_LDG = 1,     /* warps, 16-byte LDG/STG register staging, warp index broadcast */
-  STRATA_ENGINE_TMA = 2      /* one warp per CTA, cp.async.bulk through a shared-memory ring */
+  STRATA_ENGINE_DEFAULT = 0,  /* library choice: TMA for loads, LDG for offloads (B200 measurements) */
+  STRATA_ENGINE_LDG = 1,      /* warps, 16-byte LDG/STG register staging, warp index broadcast */
+  STRATA_ENGINE_TMA = 2,      /* load: one cp.async.bulk producer warp + 4 LSU consumer warps per CTA
+                                 over a shared-memory ring; offload: as STRATA_ENGINE_TMA_BULK */
+  STRATA_ENGINE_TMA_BULK = 3, /* one warp per CTA, cp.async.bulk on both sides of the ring */
+  STRATA_ENGINE_DMA = 4       /* copy-engine gather of whole page-first host runs (cudaMemcpyBatchAsync,
+                                 4 copy streams) into a double-buffered HBM staging ring + the LDG
+                                 kernel scattering staged rows to their pages (offload: the mirror).
+                                 Needs strata_xfer.host_chunks_host. */
 };
 
 typedef struct {
@@ -118,6 +126,9 @@ typedef struct {
   const int32_t* page_offset;     /* [R] host or NULL (= 0): token offset inside the first page */
   int64_t host_chunks_len;        /* entries in host_chunks (0 = unknown: list bounds unchecked) */
   int64_t dev_pages_len;          /* entries in dev_pages   (0 = unknown) */
+  const int32_t* host_chunks_host;/* host mirror of host_chunks (same content), or NULL.  Required by
+                                     STRATA_ENGINE_DMA (the CPU issues the copy-engine gathers);
+                                     ignored by the kernel engines. */
 } strata_xfer;
 
 /* Register the host tier and bind it to the device pool described by *d.

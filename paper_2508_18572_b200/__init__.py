@@ -21,6 +21,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (STRATA_D2H, STRATA_ENGINE_DEFAULT, STRATA_ENGINE_LDG, STRATA_ENGINE_TMA,  # noqa: F401
+                   STRATA_ENGINE_TMA_BULK, STRATA_ENGINE_DMA,
                    STRATA_H2D, STRATA_HOST_HUGEPAGES, STRATA_HOST_NO_NUMA_BIND,
                    STRATA_HOST_WRITECOMBINED, STRATA_VALIDATE, PoolDesc, StrataError, Xfer, check)
 
@@ -168,7 +169,7 @@ class Requests:
                     host_chunks=hc, chunk_start=self.chunk_start.ctypes.data, dev_pages=dp,
                     page_start=self.page_start.ctypes.data, chunk_offset=self.chunk_offset.ctypes.data,
                     page_offset=self.page_offset.ctypes.data, host_chunks_len=self.host_chunks_h.size,
-                    dev_pages_len=self.dev_pages_h.size)
+                    dev_pages_len=self.dev_pages_h.size, host_chunks_host=self.host_chunks_h.ctypes.data)
 
 
 class HostPool:

@@ -28,10 +28,13 @@ STRATA_HOST_HUGEPAGES = 1
 STRATA_HOST_WRITECOMBINED = 2
 STRATA_VALIDATE = 4
 STRATA_HOST_NO_NUMA_BIND = 8
+STRATA_HOST_CUDA_ALLOC = 16
 
 STRATA_ENGINE_DEFAULT = 0
 STRATA_ENGINE_LDG = 1
 STRATA_ENGINE_TMA = 2
+STRATA_ENGINE_TMA_BULK = 3
+STRATA_ENGINE_DMA = 4
 
 STRATA_H2D = 0
 STRATA_D2H = 1
@@ -69,6 +72,7 @@ class Xfer(ctypes.Structure):
         ("num_tokens", ctypes.c_void_p), ("host_chunks", ctypes.c_void_p), ("chunk_start", ctypes.c_void_p),
         ("dev_pages", ctypes.c_void_p), ("page_start", ctypes.c_void_p), ("chunk_offset", ctypes.c_void_p),
         ("page_offset", ctypes.c_void_p), ("host_chunks_len", ctypes.c_int64), ("dev_pages_len", ctypes.c_int64),
+        ("host_chunks_host", ctypes.c_void_p),
     ]
 
 

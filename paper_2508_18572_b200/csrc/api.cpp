@@ -141,7 +141,10 @@ void free_host(strata_pool* p) {
   p->host = nullptr;
 }
 
+void free_dma(strata_pool* p);
+
 void destroy(strata_pool* p) {
+  free_dma(p);
   for (cudaEvent_t e : p->events)
     if (e) cudaEventDestroy(e);
   if (p->bitmap) cudaFree(p->bitmap);
@@ -170,7 +173,7 @@ int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan) {
   if (x->layer_begin < 0 || x->layer_begin > x->layer_end || x->layer_end > L)
     return fail(STRATA_ERR_INVALID_ARG, "layer range [%d,%d) not inside [0,%d)", x->layer_begin, x->layer_end, L);
   if (x->num_reqs < 0) return fail(STRATA_ERR_INVALID_ARG, "num_reqs < 0");
-  if (x->engine < 0 || x->engine > STRATA_ENGINE_TMA) return fail(STRATA_ERR_INVALID_ARG, "unknown engine %d", x->engine);
+  if (x->engine < 0 || x->engine > STRATA_ENGINE_DMA) return fail(STRATA_ERR_INVALID_ARG, "unknown engine %d", x->engine);
   if (x->num_ctas < 0 || x->num_ctas > 65535) return fail(STRATA_ERR_INVALID_ARG, "num_ctas out of range");
   if (x->threads < 0 || x->threads > 1024 || x->threads % 32)
     return fail(STRATA_ERR_INVALID_ARG, "threads must be a multiple of 32 in [32,1024]");
@@ -242,7 +245,7 @@ int ilog2_exact(int v) {
 // Defaults chosen on B200 measurements: both engines saturate the PCIe Gen5 link
 // with a small SM quota.
 constexpr int kDefaultCtasLdg = 8;
-constexpr int kDefaultThreadsLdg = 512;
+constexpr int kDefaultThreadsLdg = 1024;   // host-read throughput of an SM scales with its warps
 constexpr int kDefaultUnroll = 8;
 constexpr int kDefaultCtasTma = 8;
 constexpr int kTmaStageTarget = 32 << 10;
@@ -295,6 +298,258 @@ bool env_validate() {
   return v && *v && strcmp(v, "0") != 0;
 }
 
+// -------------------------------------------------------------------------------------------------
+// STRATA_ENGINE_DMA: copy engines move whole page-first runs, an SM kernel does the scatter.
+//
+// The page-first host tier keeps, for one layer, the K rows and then the V rows of a chunk's C
+// tokens back to back (R1), so a layer of a fully covered chunk is ONE contiguous 2*C*S_tok run
+// (256 KiB for Llama-8B at C=64).  The copy engines read such runs at up to 98 % of the link
+// (cudaMemcpyBatchAsync of 256 KiB copies over 4 streams, profiles/r01/ce_probe.jsonl) where
+// SM-issued reads top out at 92.6 %.  Each run lands in an HBM staging slot laid out exactly like
+// a compact host tier with one layer (slot j = [K rows][V rows] of C tokens), so the unchanged LDG
+// kernel scatters it to the pages with chunk index = slot index.  Two slots alternate so the copy
+// engines fill one while the SMs scatter the other.
+struct ChunkPos {
+  int32_t req;      // request index
+  int32_t cq;       // position in the request's chunk list
+  int32_t lo, cnt;  // tokens [lo, lo+cnt) of the chunk
+  int32_t i0;       // index of the first of them within the request
+};
+
+struct Piece {
+  size_t first, count;  // chunk positions [first, first+count) -> staging slots 0..count-1
+};
+
+constexpr size_t kStageTarget = size_t(64) << 20;   // bytes per staging slot
+constexpr int kDefaultCtasScatter = 32;
+
+int ensure_dma(strata_pool* p, size_t slot_bytes, int64_t slots) {
+  cudaError_t e;
+  if (!p->cs[0]) {
+    for (auto& c : p->cs)
+      if ((e = cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking))) return cuda_fail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+    for (int s = 0; s < 2; ++s) {
+      if ((e = cudaEventCreateWithFlags(&p->ev_slot[s], cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+      for (auto& ev : p->ev_copy[s])
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  if (p->stage_bytes < slot_bytes) {
+    for (auto& b : p->stage) {
+      if (b) cudaFree(b);
+      b = nullptr;
+    }
+    p->stage_bytes = 0;
+    for (auto& b : p->stage)
+      if ((e = cudaMalloc(&b, slot_bytes))) return fail(STRATA_ERR_OOM, "cudaMalloc(staging %zu): %s", slot_bytes,
+                                                        cudaGetErrorString(e));
+    p->stage_bytes = slot_bytes;
+  }
+  if (p->slot_cap < slots) {
+    if (p->slot_ids) cudaFree(p->slot_ids);
+    p->slot_ids = nullptr;
+    p->slot_cap = 0;
+    std::vector<int32_t> iota(static_cast<size_t>(slots));
+    for (int64_t i = 0; i < slots; ++i) iota[i] = static_cast<int32_t>(i);
+    if ((e = cudaMalloc(&p->slot_ids, iota.size() * 4))) return cuda_fail(e, "cudaMalloc(slot ids)");
+    if ((e = cudaMemcpy(p->slot_ids, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice)))
+      return cuda_fail(e, "cudaMemcpy(slot ids)");
+    p->slot_cap = slots;
+  }
+  return STRATA_OK;
+}
+
+void free_dma(strata_pool* p) {
+  for (auto& b : p->stage)
+    if (b) cudaFree(b);
+  if (p->slot_ids) cudaFree(p->slot_ids);
+  for (auto& c : p->cs)
+    if (c) cudaStreamDestroy(c);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  for (int s = 0; s < 2; ++s) {
+    if (p->ev_slot[s]) cudaEventDestroy(p->ev_slot[s]);
+    for (auto& ev : p->ev_copy[s])
+      if (ev) cudaEventDestroy(ev);
+  }
+}
+
+// Submit a copy list over the pool's copy streams (contiguous shares, one batch call each).
+cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sz,
+                          int dir, int slot) {
+  cudaMemcpyAttributes attr;
+  memset(&attr, 0, sizeof attr);
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.srcLocHint.type = dir == 0 ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
+  attr.srcLocHint.id = dir == 0 ? 0 : p->d.device;
+  attr.dstLocHint.type = dir == 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
+  attr.dstLocHint.id = dir == 0 ? p->d.device : 0;
+  const size_t n = dst.size();
+  const int ns = strata_pool::kCopyStreams;
+  for (int c = 0; c < ns; ++c) {
+    const size_t lo = n * c / ns, hi = n * (c + 1) / ns;
+    if (hi > lo) {
+      size_t idx = 0, fail_idx = 0;
+      cudaError_t e = cudaMemcpyBatchAsync(dst.data() + lo, src.data() + lo, sz.data() + lo, hi - lo, &attr, &idx, 1,
+                                           &fail_idx, p->cs[c]);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(p->ev_copy[slot][c], p->cs[c]);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata::XferParams xp, cudaStream_t s,
+                 int dir, int slot_ev) {
+  if (!x->host_chunks_host) return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
+  const int64_t C = p->d.chunk_tokens, P = p->d.page_size, tok = p->tok_bytes;
+  const int L = p->d.num_layers;
+  // chunk positions of the call, request by request
+  std::vector<ChunkPos> pos;
+  for (int32_t r : plan.reqs) {
+    const int64_t n = x->num_tokens[r];
+    const int64_t oc = x->chunk_offset ? x->chunk_offset[r] : 0;
+    int64_t i = 0;
+    for (int32_t cq = 0; i < n; ++cq) {
+      const int64_t lo = cq == 0 ? oc : 0;
+      const int64_t cnt = std::min(C - lo, n - i);
+      const int64_t hc = x->host_chunks_host[x->chunk_start[r] + cq];
+      if (hc < 0 || hc >= p->d.num_chunks) return fail(STRATA_ERR_INDEX_RANGE, "host chunk %lld out of range", (long long)hc);
+      pos.push_back({r, cq, static_cast<int32_t>(lo), static_cast<int32_t>(cnt), static_cast<int32_t>(i)});
+      i += cnt;
+    }
+  }
+  const size_t unit = static_cast<size_t>(2 * C * tok);             // one chunk-layer: K rows, V rows
+  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), kStageTarget / unit));
+  // pieces: <= per_piece chunk positions and <= kMaxReqsPerLaunch requests each
+  std::vector<Piece> pieces;
+  for (size_t k = 0; k < pos.size();) {
+    Piece pc{k, 0};
+    int nreq = 0;
+    int32_t last = -1;
+    while (k < pos.size() && pc.count < per_piece) {
+      if (pos[k].req != last) {
+        if (nreq == kMaxReqsPerLaunch) break;
+        ++nreq;
+        last = pos[k].req;
+      }
+      ++pc.count;
+      ++k;
+    }
+    pieces.push_back(pc);
+  }
+  int rc = ensure_dma(p, per_piece * unit, static_cast<int64_t>(per_piece));
+  if (rc) return rc;
+
+  cudaError_t e;
+  const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
+  const int unroll = threads > 512 ? 4 : kDefaultUnroll;
+  xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows
+  const int ctas = x->num_ctas ? x->num_ctas : kDefaultCtasScatter;
+  xp.chunk_bytes = static_cast<int64_t>(unit);
+  xp.layer_off = 0;
+  xp.kv_off = C * tok;
+  xp.host_chunks = p->slot_ids;
+
+  if ((e = cudaEventRecord(p->ev_fork, s))) return cuda_fail(e, "cudaEventRecord");
+  for (auto c : p->cs)
+    if ((e = cudaStreamWaitEvent(c, p->ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+  std::vector<void*> dst, src;
+  std::vector<size_t> sz;
+  int64_t i = 0;
+  int last_slot = 0;
+  for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
+    xp.kbase = static_cast<char*>(p->k[l]);
+    xp.vbase = static_cast<char*>(p->v[l]);
+    for (const Piece& pc : pieces) {
+      const int slot = static_cast<int>(i & 1);
+      char* stage = p->stage[slot];
+      // copy list of this piece for layer l (host <-> staging slot)
+      dst.clear();
+      src.clear();
+      sz.clear();
+      for (size_t j = 0; j < pc.count; ++j) {
+        const ChunkPos& cp = pos[pc.first + j];
+        const int64_t hc = x->host_chunks_host[x->chunk_start[cp.req] + cp.cq];
+        char* h = p->host + hc * p->chunk_bytes + int64_t(l) * 2 * C * tok;
+        char* d = stage + j * unit;
+        auto add = [&](int64_t off, int64_t bytes) {
+          dst.push_back(dir == 0 ? d + off : h + off);
+          src.push_back(dir == 0 ? h + off : d + off);
+          sz.push_back(static_cast<size_t>(bytes));
+        };
+        if (cp.lo == 0 && cp.cnt == C) {
+          add(0, 2 * C * tok);                         // K and V runs are adjacent: one copy
+        } else {
+          add(cp.lo * tok, cp.cnt * tok);              // K rows
+          add((C + cp.lo) * tok, cp.cnt * tok);        // V rows
+        }
+      }
+      // request table of the piece: sub-requests addressing staging slots
+      strata::ReqTable& rt = xp.rt;
+      rt.n = 0;
+      int32_t acc = 0;
+      for (size_t j = 0; j < pc.count; ++j) {
+        const ChunkPos& cp = pos[pc.first + j];
+        if (j == 0 || cp.req != pos[pc.first + j - 1].req) {
+          const int k = rt.n++;
+          const int64_t op = x->page_offset ? x->page_offset[cp.req] : 0;
+          const int64_t pi0 = op + cp.i0;
+          rt.tok_end[k] = acc;
+          rt.chunk_base[k] = static_cast<int32_t>(j);
+          rt.off_c[k] = cp.lo;
+          rt.page_base[k] = static_cast<int32_t>(x->page_start[cp.req] + pi0 / P);
+          rt.off_p[k] = static_cast<int32_t>(pi0 % P);
+        }
+        acc += cp.cnt;
+        rt.tok_end[rt.n - 1] = acc;
+      }
+      xp.ntok = acc;
+      xp.host = stage;
+      const int64_t groups = (2LL * acc + xp.rows_per_group - 1) / xp.rows_per_group;
+      const int c = static_cast<int>(std::min<int64_t>(ctas, (groups * 32 + threads - 1) / threads));
+      if (dir == 0) {
+        // copies into the slot (after its previous scatter), then the scatter on the caller's stream
+        if (i >= 2)
+          for (auto cs : p->cs)
+            if ((e = cudaStreamWaitEvent(cs, p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        for (auto ev : p->ev_copy[slot])
+          if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = strata::launch_ldg(xp, 0, c, threads, unroll, s))) return cuda_fail(e, "scatter kernel launch");
+        if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
+      } else {
+        // gather into the slot (after its previous copies drained), then copies to the host tier
+        if (i >= 2)
+          for (auto ev : p->ev_copy[slot])
+            if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = strata::launch_ldg(xp, 1, c, threads, unroll, s))) return cuda_fail(e, "gather kernel launch");
+        if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
+        for (auto cs : p->cs)
+          if ((e = cudaStreamWaitEvent(cs, p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+      }
+      last_slot = slot;
+      ++i;
+    }
+    cudaEvent_t lev = p->events[size_t(slot_ev) * (L + 1) + 1 + l];
+    if (dir == 0) {
+      e = cudaEventRecord(lev, s);
+    } else {
+      // host bytes of layer l are written once every copy stream has passed the layer's last piece
+      for (int c = 1; c < strata_pool::kCopyStreams; ++c)
+        if ((e = cudaStreamWaitEvent(p->cs[0], p->ev_copy[last_slot][c], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+      e = cudaEventRecord(lev, p->cs[0]);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  }
+  if (dir == 1 && i > 0)  // join: the caller's stream is ordered after every copy
+    for (auto ev : p->ev_copy[last_slot])
+      if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+  return STRATA_OK;
+}
+
 int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir) {
   if (!p) return fail(STRATA_ERR_INVALID_ARG, "pool is NULL");
   Plan plan;
@@ -319,6 +574,8 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.vpt = xp.tok_bytes / 16;
   xp.vpt_shift = ilog2_exact(xp.vpt);
   xp.vph = xp.head_bytes / 16;
+  xp.c_shift = ilog2_exact(xp.C);
+  xp.p_shift = ilog2_exact(xp.P);
   xp.chunk_bytes = p->chunk_bytes;
   xp.kv_off = int64_t(p->d.chunk_tokens) * p->tok_bytes;
   xp.page_stride = p->page_stride;
@@ -328,9 +585,24 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.host_chunks = x->host_chunks;
   xp.dev_pages = x->dev_pages;
 
-  int engine = x->engine == STRATA_ENGINE_DEFAULT ? STRATA_ENGINE_TMA : x->engine;
+  int engine = x->engine;
+  if (engine == STRATA_ENGINE_DEFAULT) engine = dir == 0 ? STRATA_ENGINE_TMA : STRATA_ENGINE_LDG;
+  if (engine == STRATA_ENGINE_DMA) {
+    if (!x->host_chunks_host && plan.total_tokens > 0)
+      return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
+    const uint64_t t = p->next_ticket++;
+    const int slot = static_cast<int>(t % kEventRing);
+    p->ops[slot] = {t, x->layer_begin, x->layer_end};
+    e = cudaEventRecord(p->events[size_t(slot) * (p->d.num_layers + 1)], s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    rc = transfer_dma(p, x, plan, xp, s, dir, slot);
+    if (rc) return rc;
+    if (ticket) *ticket = t;
+    return STRATA_OK;
+  }
+  const bool tma = engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK;
   // TMA engine geometry: rows per stage (<= 32 lanes), stage bytes, depth
-  if (engine == STRATA_ENGINE_TMA) {
+  if (tma) {
     int rows = std::max(1, std::min(32, kTmaStageTarget / xp.tok_bytes));
     const int sb = rows * xp.tok_bytes;
     const int budget = p->tma_smem - strata::tma_header_bytes(strata::kTmaMaxStages);
@@ -343,10 +615,10 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
       xp.tma_stages = stages;
     }
   }
-  const int unroll = kDefaultUnroll;
-  xp.rows_per_group = std::max(1, std::min(32, (32 * unroll) / std::max(1, xp.vpt)));
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
-  int ctas = x->num_ctas ? x->num_ctas : (engine == STRATA_ENGINE_TMA ? kDefaultCtasTma : kDefaultCtasLdg);
+  const int unroll = threads > 512 ? 4 : kDefaultUnroll;   // U=8 is compiled for <= 512 threads
+  xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows (amortised index math)
+  int ctas = x->num_ctas ? x->num_ctas : (engine == STRATA_ENGINE_LDG ? kDefaultCtasLdg : kDefaultCtasTma);
 
   const uint64_t t = p->next_ticket++;
   const int slot = static_cast<int>(t % kEventRing);
@@ -363,10 +635,10 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
       fill_table(x, plan, b, xp.rt);
       const int64_t rows = 2LL * b.ntok;
       int c = ctas;
-      if (engine == STRATA_ENGINE_TMA) {
+      if (engine != STRATA_ENGINE_LDG) {
         const int64_t pieces = (rows + xp.tma_rows - 1) / xp.tma_rows;
         if (pieces < c) c = static_cast<int>(pieces);
-        e = strata::launch_tma(xp, dir, c, s);
+        e = strata::launch_tma(xp, dir, c, engine == STRATA_ENGINE_TMA, s);
       } else {
         const int64_t groups = (rows + xp.rows_per_group - 1) / xp.rows_per_group;
         const int64_t need = (groups * 32 + threads - 1) / threads;
@@ -444,13 +716,15 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
     } else {
       p->registered_by_us = true;
     }
-  } else if (d->flags & STRATA_HOST_WRITECOMBINED) {
+  } else if (d->flags & (STRATA_HOST_WRITECOMBINED | STRATA_HOST_CUDA_ALLOC)) {
     void* h = nullptr;
-    e = cudaHostAlloc(&h, p->host_bytes, cudaHostAllocMapped | cudaHostAllocPortable | cudaHostAllocWriteCombined);
+    unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
+    if (d->flags & STRATA_HOST_WRITECOMBINED) fl |= cudaHostAllocWriteCombined;
+    e = cudaHostAlloc(&h, p->host_bytes, fl);
     if (e != cudaSuccess) {
       const size_t want = p->host_bytes;
       delete p;
-      return fail(STRATA_ERR_OOM, "cudaHostAlloc(%zu, write-combined): %s", want, cudaGetErrorString(e));
+      return fail(STRATA_ERR_OOM, "cudaHostAlloc(%zu, flags %u): %s", want, fl, cudaGetErrorString(e));
     }
     p->host = static_cast<char*>(h);
     p->host_kind = 2;

@@ -41,6 +41,7 @@ struct XferParams {
   int32_t tma_rows;             // TMA engine: token rows per pipeline stage (<= 32)
   int32_t tma_stages;           // TMA engine: pipeline depth
   int32_t tma_stage_bytes;      // TMA engine: bytes per stage (>= tma_rows * tok_bytes)
+  int32_t c_shift, p_shift;     // log2(C), log2(P) when powers of two, else -1
   int64_t chunk_bytes;          // L*2*C*S_tok
   int64_t layer_off;            // byte offset of (layer, K) inside a host chunk: l*2*C*S_tok
   int64_t kv_off;               // byte offset from K to V inside a chunk layer: C*S_tok
@@ -71,7 +72,8 @@ struct ValidateParams {
 
 // Kernel launchers (kernels.cu).  dir: 0 = load (host -> device), 1 = offload (device -> host).
 cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s);
-cudaError_t launch_tma(const XferParams& p, int dir, int ctas, cudaStream_t s);
+// warp_specialized (load only): 1 TMA producer warp + LSU consumer warps; else one bulk-only warp.
+cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s);
 cudaError_t launch_validate(const ValidateParams& v, cudaStream_t s);
 // Largest dynamic shared memory the TMA engine may use per CTA on this device.
 int tma_smem_limit();
@@ -109,4 +111,14 @@ struct strata_pool {
   int32_t* err_dev = nullptr;
   int32_t* err_host = nullptr;        // pinned
   int tma_smem = 0;
+  // STRATA_ENGINE_DMA: double-buffered HBM staging ring, copy streams and their events (lazy)
+  static constexpr int kCopyStreams = 4;
+  char* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;             // bytes per staging slot
+  int32_t* slot_ids = nullptr;        // device iota [0, slot_cap): chunk index of each staging slot
+  int64_t slot_cap = 0;
+  cudaStream_t cs[kCopyStreams] = {};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_slot[2] = {nullptr, nullptr};                 // staging slot reusable
+  cudaEvent_t ev_copy[2][kCopyStreams] = {};                   // a slot's copies done, per stream
 };

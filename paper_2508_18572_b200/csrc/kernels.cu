@@ -43,21 +43,47 @@ __device__ __forceinline__ int find_req(const ReqTable& rt, int32_t g) {
   return lo;
 }
 
-__device__ __forceinline__ void row_addr(const XferParams& p, int64_t row, char*& hp, char*& dp) {
-  const int kv = row >= p.ntok;
-  const int32_t g = static_cast<int32_t>(row - (kv ? p.ntok : 0));
+// The index fetch is split in two so kernels can software-pipeline it: row_fetch issues the two
+// int32 index loads (page table, chunk list) for a row and returns at once; row_finish, called an
+// iteration later when the loads have landed, applies the layout transform.  This keeps the
+// index-load latency (~0.5-1 us from L2/HBM) off the critical path of each pipeline iteration.
+struct RowIdx {
+  int32_t hc, pg;     // host chunk index, device page index (loaded)
+  int32_t cr, pr;     // token position inside the chunk / page
+  int32_t kv;         // 0 = K row, 1 = V row; -1 = no row
+};
+
+__device__ __forceinline__ RowIdx row_fetch(const XferParams& p, int64_t row) {
+  RowIdx x;
+  x.kv = row >= p.ntok;
+  const int32_t g = static_cast<int32_t>(row - (x.kv ? p.ntok : 0));
   const int r = find_req(p.rt, g);
   const int32_t i = g - (r ? p.rt.tok_end[r - 1] : 0);
   const int32_t ci = p.rt.off_c[r] + i;         // position in the request's host chunk list
   const int32_t pi = p.rt.off_p[r] + i;         // position in the request's device page list
-  const int32_t cq = ci / p.C, cr = ci - cq * p.C;
-  const int32_t pq = pi / p.P, pr = pi - pq * p.P;
-  const int64_t hc = __ldg(p.host_chunks + p.rt.chunk_base[r] + cq);
-  const int64_t pg = __ldg(p.dev_pages + p.rt.page_base[r] + pq);
+  const int32_t cq = p.c_shift >= 0 ? (ci >> p.c_shift) : ci / p.C;
+  const int32_t pq = p.p_shift >= 0 ? (pi >> p.p_shift) : pi / p.P;
+  x.cr = ci - cq * p.C;
+  x.pr = pi - pq * p.P;
+  x.hc = __ldg(p.host_chunks + p.rt.chunk_base[r] + cq);
+  x.pg = __ldg(p.dev_pages + p.rt.page_base[r] + pq);
+  return x;
+}
+
+__device__ __forceinline__ RowIdx row_none() {
+  RowIdx x;
+  x.hc = x.pg = x.cr = x.pr = 0;
+  x.kv = -1;
+  return x;
+}
+
+__device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x, char*& hp, char*& dp) {
   // host: chunk hc, layer l, kv, token cr            (page-first)
-  hp = p.host + hc * p.chunk_bytes + p.layer_off + kv * p.kv_off + static_cast<int64_t>(cr) * p.tok_bytes;
+  hp = p.host + static_cast<int64_t>(x.hc) * p.chunk_bytes + p.layer_off + x.kv * p.kv_off +
+       static_cast<int64_t>(x.cr) * p.tok_bytes;
   // device: page pg, offset pr of this layer's K/V  (layer-first paged pool)
-  dp = (kv ? p.vbase : p.kbase) + pg * p.page_stride + static_cast<int64_t>(pr) * p.token_stride;
+  dp = (x.kv ? p.vbase : p.kbase) + static_cast<int64_t>(x.pg) * p.page_stride +
+       static_cast<int64_t>(x.pr) * p.token_stride;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -77,19 +103,28 @@ __device__ __forceinline__ void st_vec(void* ptr, const int4& v) {
 // LDG engine.  DIR 0: host -> device, DIR 1: device -> host.  CONTIG: device rows head-contiguous
 // (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
 template <int U, bool CONTIG, int DIR>
-__global__ void __launch_bounds__(1024) ldg_kernel(const __grid_constant__ XferParams p) {
+__global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __grid_constant__ XferParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int64_t nrows = 2LL * p.ntok;
   const int RG = p.rows_per_group;
   const int64_t ngroups = (nrows + RG - 1) / RG;
+  // lane t fetches row t of the group; the next group's fetch is issued before this group's data
+  // loads so its latency hides under them
+  auto fetch = [&](int64_t gi) {
+    const int64_t row = gi * RG + lane;
+    return (gi < ngroups && lane < RG && row < nrows) ? row_fetch(p, row) : row_none();
+  };
+  RowIdx nx = fetch(warp);
   for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
     const int64_t row0 = gi * RG;
     const int nr = static_cast<int>(min(static_cast<int64_t>(RG), nrows - row0));
+    const RowIdx cur = nx;
+    nx = fetch(gi + nwarps);
     char* hp = nullptr;
     char* dp = nullptr;
-    if (lane < nr) row_addr(p, row0 + lane, hp, dp);   // index fetch by lane, broadcast below
+    if (cur.kv >= 0) row_finish(p, cur, hp, dp);   // addresses by lane, broadcast below
     const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
     const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
     const int nvec = nr * p.vpt;
@@ -167,7 +202,7 @@ __device__ __forceinline__ void bulk_wait_read1() {
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-constexpr int kTmaHeader = 8 * kTmaMaxStages;            // mbarriers
+constexpr int kTmaHeader = 16 * kTmaMaxStages;           // mbarriers: full[32], empty[32]
 
 __host__ __device__ constexpr int tma_table_bytes(int stages) { return stages * 32 * 12; }
 __host__ __device__ constexpr int tma_buf_offset(int stages) {
@@ -199,13 +234,18 @@ __global__ void __launch_bounds__(32, 1) tma_kernel(const __grid_constant__ Xfer
   const int64_t npieces = (nrows + T - 1) / T;
   const int64_t my = npieces > blockIdx.x ? (npieces - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  auto issue = [&](int64_t k) {
-    const int s = static_cast<int>(k % S);
+  // index fetch for piece k (issued one pipeline step ahead of its use, see row_fetch)
+  auto fetch = [&](int64_t k) {
     const int64_t row = (blockIdx.x + k * gridDim.x) * T + lane;
-    const bool valid = lane < T && row < nrows;
+    return (k < my && lane < T && row < nrows) ? row_fetch(p, row) : row_none();
+  };
+
+  auto issue = [&](int64_t k, const RowIdx& x) {
+    const int s = static_cast<int>(k % S);
+    const bool valid = x.kv >= 0;
     char* hp = nullptr;
     char* dp = nullptr;
-    if (valid) row_addr(p, row, hp, dp);
+    if (valid) row_finish(p, x, hp, dp);
     // host-side runs: a lane starts a run unless its row directly follows the previous lane's
     const uint64_t hprev = __shfl_up_sync(kFull, reinterpret_cast<uint64_t>(hp), 1);
     const int vprev = __shfl_up_sync(kFull, static_cast<int>(valid), 1);
@@ -261,17 +301,133 @@ __global__ void __launch_bounds__(32, 1) tma_kernel(const __grid_constant__ Xfer
   };
 
   const int64_t pro = my < S ? my : S;
-  for (int64_t k = 0; k < pro; ++k) issue(k);
+  RowIdx nx = fetch(0);
+  for (int64_t k = 0; k < pro; ++k) {
+    const RowIdx cur = nx;
+    nx = fetch(k + 1);
+    issue(k, cur);
+  }
   for (int64_t k = 0; k < my; ++k) {
     consume(k);
     // refill the stage piece k-1 used once its stores have read shared memory
     if (k >= 1 && k - 1 + S < my) {
+      const RowIdx cur = nx;          // fetched one step ago: piece k-1+S
+      nx = fetch(k + S);
       bulk_wait_read1();
       __syncwarp();
-      issue(k - 1 + S);
+      issue(k - 1 + S, cur);
     }
   }
   bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Warp-specialised TMA load (the default load engine).  Warp 0 is the producer: it fetches the
+// indices of a piece (software-pipelined one piece ahead), publishes each row's device address in a
+// per-stage table, and issues ONE cp.async.bulk per contiguous host run into the stage.  Warps
+// 1..kWsConsumers drain a full stage to the pages with ld.shared.v4 / st.global.v4 (16-byte
+// vectors, any page size or head stride) and release it on the stage's `empty` mbarrier.  The TMA
+// unit only sees large contiguous host reads; the scattered small writes go through the LSU, so one
+// SM sustains ~45 GB/s of host reads and two saturate the PCIe link (the paper's 2-CTA quota,
+// PAPER.md:262).
+constexpr int kWsConsumers = 4;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ int4 ld_shared_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+
+template <bool CONTIG>
+__global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel(const __grid_constant__ XferParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.tma_stages;
+  const int T = p.tma_rows;
+  const int SB = p.tma_stage_bytes;
+  const int tok = p.tok_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kTmaMaxStages;
+  uint64_t* tab_addr = reinterpret_cast<uint64_t*>(smem + kTmaHeader);   // [S][32] device row address
+  unsigned char* buf = smem + tma_buf_offset(S);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWsConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t nrows = 2LL * p.ntok;
+  const int64_t npieces = (nrows + T - 1) / T;
+  const int64_t my = npieces > blockIdx.x ? (npieces - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    auto fetch = [&](int64_t k) {
+      const int64_t row = (blockIdx.x + k * gridDim.x) * T + lane;
+      return (k < my && lane < T && row < nrows) ? row_fetch(p, row) : row_none();
+    };
+    RowIdx nx = fetch(0);
+    for (int64_t k = 0; k < my; ++k) {
+      const int s = static_cast<int>(k % S);
+      const RowIdx cur = nx;
+      nx = fetch(k + 1);
+      if (k >= S) mbar_wait(&empty[s], static_cast<uint32_t>(((k / S) - 1) & 1));
+      const bool valid = cur.kv >= 0;
+      char* hp = nullptr;
+      char* dp = nullptr;
+      if (valid) row_finish(p, cur, hp, dp);
+      const uint64_t hprev = __shfl_up_sync(kFull, reinterpret_cast<uint64_t>(hp), 1);
+      const int vprev = __shfl_up_sync(kFull, static_cast<int>(valid), 1);
+      const bool head = valid && !(lane > 0 && vprev && hprev + tok == reinterpret_cast<uint64_t>(hp));
+      const unsigned heads = __ballot_sync(kFull, head);
+      const int nvalid = __popc(__ballot_sync(kFull, valid));
+      const unsigned later = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
+      const int run = (later ? __ffs(later) - 1 : nvalid) - lane;
+      tab_addr[s * 32 + lane] = reinterpret_cast<uint64_t>(dp);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nvalid * tok));
+      __syncwarp();
+      if (head) bulk_g2s(buf + static_cast<size_t>(s) * SB + lane * tok, hp, static_cast<uint32_t>(run * tok),
+                         &full[s]);
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const int ct = threadIdx.x - 32;
+    constexpr int kThreads = 32 * kWsConsumers;
+    const int nvec = T * p.vpt;
+    for (int64_t k = 0; k < my; ++k) {
+      const int s = static_cast<int>(k % S);
+      mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
+      const unsigned char* st = buf + static_cast<size_t>(s) * SB;
+      const uint64_t* tab = tab_addr + s * 32;
+#pragma unroll 4
+      for (int vi = ct; vi < nvec; vi += kThreads) {
+        const int row = p.vpt_shift >= 0 ? (vi >> p.vpt_shift) : (vi / p.vpt);
+        const int w = vi - row * p.vpt;
+        char* d = reinterpret_cast<char*>(tab[row]);
+        if (d) {
+          const int4 val = ld_shared_v4(st + row * tok + w * 16);
+          if (CONTIG) {
+            st_vec(d + w * 16, val);
+          } else {
+            const int h = w / p.vph;
+            st_vec(d + h * p.head_stride + (w - h * p.vph) * 16, val);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -324,6 +480,7 @@ cudaError_t tma_launch(const XferParams& p, int ctas, cudaStream_t s) {
 
 cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s) {
   const bool contig = p.head_stride == p.head_bytes;
+  if (threads > 512) unroll = 4;  // U=8 needs > 64 registers per thread
 #define STRATA_LDG(U)                                                               \
   if (unroll == U) {                                                                \
     if (dir == 0) return contig ? ldg_launch<U, true, 0>(p, ctas, threads, s)       \
@@ -337,8 +494,14 @@ cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int 
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_tma(const XferParams& p, int dir, int ctas, cudaStream_t s) {
+cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s) {
   const bool contig = p.head_stride == p.head_bytes;
+  if (dir == 0 && warp_specialized) {
+    const int smem = tma_buf_offset(p.tma_stages) + p.tma_stages * p.tma_stage_bytes;
+    if (contig) tma_ws_load_kernel<true><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
+    else tma_ws_load_kernel<false><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
+    return cudaGetLastError();
+  }
   if (dir == 0) return contig ? tma_launch<0, true>(p, ctas, s) : tma_launch<0, false>(p, ctas, s);
   return contig ? tma_launch<1, true>(p, ctas, s) : tma_launch<1, false>(p, ctas, s);
 }
@@ -363,6 +526,8 @@ int tma_header_bytes(int stages) { return tma_buf_offset(stages); }
 
 cudaError_t tma_prepare(int smem) {
   cudaError_t e;
+  if ((e = cudaFuncSetAttribute(tma_ws_load_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(tma_ws_load_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;

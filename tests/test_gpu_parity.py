@@ -18,7 +18,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU box
 
 import paper_2508_18572_b200 as st  # noqa: E402
 
-ENGINES = [st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_TMA]
+ENGINES = [st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_TMA_BULK, st.STRATA_ENGINE_DMA]
 
 
 def _sync():
@@ -60,7 +60,7 @@ def _fuzz_params(i):
     if rng.random() < 0.2:
         l0, l1 = 0, L
     ctas = int(rng.choice([0, 1, 2, 4, 16, 148]))
-    engine = ENGINES[i % 2]
+    engine = ENGINES[i % len(ENGINES)]
     frag = "churn" if rng.random() < 0.3 else "perm"
     layout = rng.choice(["nhd", "hnd", "padded"])
     return dict(rng=rng, L=L, H=H, D=D, e=e, P=P, C=C, ns=ns, l0=l0, l1=l1, ctas=ctas, engine=engine,
@@ -149,6 +149,42 @@ def test_special_float_payloads(engine):
         c.pool.load(c.reqs, engine=engine)
         _sync()
         c.check_load(0, g.L)
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("direction", ["load", "offload"])
+def test_dma_engine_multi_piece(direction):
+    """STRATA_ENGINE_DMA with layers larger than one 64 MiB staging slot: several pieces per layer
+    alternate between the two slots, within and across layers; partial first/last chunks."""
+    g = Geometry(6, 8, 128, 2, 1, 64, 40960, 560)
+    rng = kvgen.rng_for(21)
+    q = kvgen.make_requests(rng, [20000, 13000, 77], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
+    c = GpuCase(g, q, dev_fill="canary" if direction == "load" else "random")
+    try:
+        if direction == "load":
+            c.pool.load(c.reqs, 1, 6, engine=st.STRATA_ENGINE_DMA)
+            _sync()
+            c.check_load(1, 6)
+        else:
+            before = c.pool.host.copy()
+            c.pool.offload(c.reqs, 0, 5, engine=st.STRATA_ENGINE_DMA)
+            _sync()
+            assert np.array_equal(c.pool.host, c.expected_offload(before, 0, 5))
+    finally:
+        c.close()
+
+
+def test_dma_engine_needs_host_list():
+    g = kvgen.geometry("tiny")
+    q = kvgen.make_requests(kvgen.rng_for(0), [64], g.P, g.C, g.num_pages, g.num_chunks)
+    c = GpuCase(g, q)
+    try:
+        x = c.reqs.xfer(0, g.L, engine=st.STRATA_ENGINE_DMA)
+        x.host_chunks_host = None
+        with pytest.raises(st.StrataError) as e:
+            st.strata_load(c.pool.handle, x)
+        assert e.value.code == st._lib.STRATA_ERR_INVALID_ARG
     finally:
         c.close()
 

@@ -1,0 +1,125 @@
+#!/usr/bin/env python
+"""Interference-aware SM quota (§4.2, fig:interference).
+
+The paper co-runs its I/O kernel with a prefill pass (2 requests x 4K) and a decode pass (16 requests
+x 4K) on H200 and picks 2 CTAs x 1024 threads for loads (~50 GB/s, < 5 % prefill and < 10 % decode
+slowdown) and 1 CTA for backups.  Here the same experiment runs on B200 with synthetic proxies:
+
+  prefill proxy  bf16 GEMMs of a Llama-3.1-8B layer for 2 x 4K tokens (M=8192: QKV 4096x6144,
+                 O 4096x4096, gate/up 4096x28672, down 14336x4096) — tensor-core bound;
+  decode proxy   a read of 16 x 4K tokens of Llama-8B KV per layer for 32 layers (8 GiB, fp32-
+                 accumulated sum) — HBM bound.
+
+For each engine x SM quota (num_ctas) it measures the proxy alone, the I/O alone, and both at once
+(I/O on a high-priority stream looping strata_load over the Llama-8B 32K workload), and reports the
+proxy slowdown and the co-run I/O bandwidth.  One JSON object per line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import kvgen  # noqa: E402
+import paper_2508_18572_b200 as st  # noqa: E402
+
+
+def make_prefill():
+    M = 8192
+    shapes = [(4096, 6144), (4096, 4096), (4096, 28672), (14336, 4096)]
+    xs = {k: torch.randn(M, k, dtype=torch.bfloat16, device="cuda") for k, _ in shapes}
+    ws = [torch.randn(k, n, dtype=torch.bfloat16, device="cuda") for k, n in shapes]
+
+    def run():
+        for (k, n), w in zip(shapes, ws):
+            torch.matmul(xs[k], w)
+    return run
+
+
+def make_decode():
+    # 16 requests x 4096 tokens x 8 heads x 128 dim x bf16 x (K,V) = 256 MiB per layer, 32 layers
+    kv = [torch.randn(16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda")
+          for _ in range(32)]
+
+    def run():
+        for t in kv:
+            t.sum(dtype=torch.float32)
+    return run
+
+
+def time_proxy(fn, stream, reps):
+    evs = []
+    with torch.cuda.stream(stream):
+        fn()
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            evs.append((a, b))
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ctas", default="1,2,4,8,16")
+    ap.add_argument("--engines", default="1,2")
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+
+    g = kvgen.geometry("llama8b_32k")
+    q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks)
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+    reqs = st.Requests.from_kvgen(q)
+    bytes_load = 2 * g.L * q.total_tokens * g.token_bytes
+    lo, hi = torch.cuda.Stream.priority_range()
+    io = torch.cuda.Stream(priority=hi)       # I/O: high priority (its few CTAs get SMs first)
+    comp = torch.cuda.Stream(priority=lo)
+    proxies = {"prefill": make_prefill(), "decode": make_decode()}
+    alone = {name: time_proxy(fn, comp, args.reps) for name, fn in proxies.items()}
+    print(json.dumps({"kind": "proxy_alone", **{k_: round(v_, 4) for k_, v_ in alone.items()}}), flush=True)
+
+    for eng in [int(x) for x in args.engines.split(",")]:
+        for c in [int(x) for x in args.ctas.split(",")]:
+            # I/O alone
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            pool.load(reqs, stream=io, engine=eng, num_ctas=c)
+            a.record(io)
+            for _ in range(3):
+                pool.load(reqs, stream=io, engine=eng, num_ctas=c)
+            b.record(io)
+            b.synchronize()
+            io_alone = 3 * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
+            for name, fn in proxies.items():
+                # keep the I/O stream busy for the whole proxy measurement
+                n_loads = max(2, int(alone[name] * args.reps / (bytes_load / io_alone / 1e6)) + 2)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(io)
+                for _ in range(n_loads):
+                    pool.load(reqs, stream=io, engine=eng, num_ctas=c)
+                b.record(io)
+                t_co = time_proxy(fn, comp, args.reps)
+                b.synchronize()
+                io_co = n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
+                print(json.dumps({"kind": "corun", "engine": eng, "ctas": c, "proxy": name,
+                                  "proxy_alone_ms": round(alone[name], 4), "proxy_corun_ms": round(t_co, 4),
+                                  "slowdown": round(t_co / alone[name] - 1, 4), "io_alone_gbs": round(io_alone, 2),
+                                  "io_corun_gbs_upper": round(io_co, 2)}), flush=True)
+    pool.close()
+
+
+if __name__ == "__main__":
+    main()

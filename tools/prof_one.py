@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--engine", type=int, default=2)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--dir", default="h2d")
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
@@ -38,7 +39,7 @@ def main():
     reqs = st.Requests.from_kvgen(q)
     fn = pool.load if args.dir == "h2d" else pool.offload
     for _ in range(args.reps):
-        fn(reqs, engine=args.engine, num_ctas=args.ctas)
+        fn(reqs, engine=args.engine, num_ctas=args.ctas, threads=args.threads)
     torch.cuda.synchronize()
     pool.close()
 

@@ -51,27 +51,34 @@ def main():
     ap.add_argument("--baselines", default="1")
     ap.add_argument("--layers", type=int, default=0, help="override L (0 = config)")
     ap.add_argument("--frag", default="perm")
+    ap.add_argument("--chunk-frag", default="perm", help="host chunk order: perm | identity")
+    ap.add_argument("--flags", type=int, default=0, help="strata_pool_desc.flags (host allocation)")
+    ap.add_argument("--tag", default="")
+    ap.add_argument("--threads", type=int, default=0, help="LDG engine threads per CTA (0 = default)")
     args = ap.parse_args()
     io = torch.cuda.Stream()
     for P in [int(x) for x in args.pages.split(",")]:
         over = {"L": args.layers} if args.layers else {}
         g = kvgen.geometry(args.config, P=P, **over)
         n = kvgen.CONFIGS[args.config]["n"]
-        q = kvgen.make_requests(kvgen.rng_for(1), n, g.P, g.C, g.num_pages, g.num_chunks, frag=args.frag)
+        q = kvgen.make_requests(kvgen.rng_for(1), n, g.P, g.C, g.num_pages, g.num_chunks, frag=args.frag,
+                                chunk_frag=args.chunk_frag)
         nb = g.num_pages * g.P * g.token_bytes
         k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
         v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
         pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P,
-                           chunk_tokens=g.C, k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+                           chunk_tokens=g.C, k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks,
+                           flags=args.flags)
         kvgen.fill_random(pool.host, 3)
         reqs = st.Requests.from_kvgen(q)
         nbytes = 2 * g.L * q.total_tokens * g.token_bytes
-        base = {"config": args.config, "P": P, "L": g.L, "tokens": q.total_tokens, "bytes": nbytes, "frag": args.frag}
+        base = {"config": args.config, "P": P, "L": g.L, "tokens": q.total_tokens, "bytes": nbytes, "frag": args.frag,
+                "chunk_frag": args.chunk_frag, "flags": args.flags, "tag": args.tag}
         for eng in [int(x) for x in args.engines.split(",")]:
             for c in [int(x) for x in args.ctas.split(",")]:
                 for d, fn in (("h2d", pool.load), ("d2h", pool.offload)):
-                    ev, wall = timed(lambda: fn(reqs, stream=io, engine=eng, num_ctas=c), io)
-                    print(json.dumps({**base, "method": "strata", "dir": d, "engine": eng, "ctas": c,
+                    ev, wall = timed(lambda: fn(reqs, stream=io, engine=eng, num_ctas=c, threads=args.threads), io)
+                    print(json.dumps({**base, "method": "strata", "dir": d, "engine": eng, "ctas": c, "threads": args.threads,
                                       "ms": round(ev * 1e3, 3), "wall_ms": round(wall * 1e3, 3),
                                       "gbs": round(nbytes / ev / 1e9, 3)}), flush=True)
         if args.baselines == "1":
