@@ -32,6 +32,14 @@ import numpy as np  # noqa: E402
 import kvgen  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+ENGINE_NAMES = {0: "default", 1: "ldg", 2: "tma", 3: "tma_bulk", 4: "dma"}
+PATH_DESC = {
+    "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (cudaMemcpyBatchAsync, 4 streams) "
+           "into an HBM staging slot + ldg_kernel scatter to the pages; one event per layer",
+    "ldg": "ldg_kernel, zero-copy LDG/STG from mapped host memory, one launch + event per layer",
+    "tma": "tma_ws_load_kernel, zero-copy cp.async.bulk ring, one launch + event per layer",
+    "tma_bulk": "tma_kernel, zero-copy cp.async.bulk ring, one launch + event per layer",
+}
 
 
 def parse():
@@ -230,6 +238,7 @@ def main():
     barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    c0 = pool.counters()
     with ClockSampler(local) as clocks:
         start.record(io)
         last = None
@@ -239,6 +248,9 @@ def main():
         marks[-1].record(io)
         end.record(io)
         barrier()
+    c1 = pool.counters()
+    launches = c1["kernel_launches"] - c0["kernel_launches"]
+    engine_used = ENGINE_NAMES.get(c1["last_engine"], str(c1["last_engine"]))
     elapsed = start.elapsed_time(end) / 1e3
     step_ms = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps))
     step_stats = {"median_ms": round(statistics.median(step_ms), 3),
@@ -295,6 +307,20 @@ def main():
     e2e_value = bytes_step * world * e2e_steps / float(te.item()) / 1e9
     h2d = bytes_step + 4 * (reqs.host_chunks_h.size + reqs.dev_pages_h.size)
 
+    # the other engines on the same workload, default SM quota, for comparison in the same line
+    others = {}
+    for eng in (st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_DMA):
+        if ENGINE_NAMES[eng] == engine_used:
+            continue
+        pool.load(reqs, 0, g.L, stream=io, engine=eng)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(io)
+        for _ in range(3):
+            pool.load(reqs, 0, g.L, stream=io, engine=eng)
+        b.record(io)
+        b.synchronize()
+        others[ENGINE_NAMES[eng]] = round(3 * bytes_step / (a.elapsed_time(b) / 1e3) / 1e9, 3)
+
     out = None
     if rank == 0:
         per_launch_bytes = bytes_step // g.L
@@ -303,7 +329,8 @@ def main():
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(f"{args.config}_P{g.P}")
+            traffic = json.load(open(tp)).get(f"{args.config}_P{g.P}_{engine_used}")
+        path = PATH_DESC.get(engine_used, engine_used)
         peaks = {}
         mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
         if os.path.exists(mp):
@@ -323,7 +350,7 @@ def main():
             "frac_of_link": round(value / world / link_peak, 4),
             "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3), "peak": round(link_peak, 3),
                          "unit": "GB/s", "frac": round(achieved / link_peak, 4), "traffic": traffic,
-                         "kernel": "strata load kernel (one launch per layer)",
+                         "kernel": path,
                          "per_launch_bytes": per_launch_bytes, "avg_launch_ms": round(avg_launch, 4),
                          "peak_source": "contiguous pinned cudaMemcpyAsync H2D from the same registered host "
                                         "tier, measured in this run (PCIe Gen5 x16 nominal 64 GB/s)",
@@ -333,9 +360,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": 16},
-            "gpu_launches": args.steps * g.L * batches,
+            "gpu_launches": launches,
             "clocks": clocks.summary(),
-            "engine": args.engine, "num_ctas": args.num_ctas,
+            "engine": engine_used, "num_ctas": args.num_ctas or "default",
+            "other_engines_gbs": others,
         }
         print(json.dumps(out), flush=True)
     pool.close()

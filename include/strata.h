@@ -80,7 +80,8 @@ enum strata_pool_flags {
 
 /* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
 enum strata_engine {
-  STRATA_ENGINE_DEFAULT = 0,  /* library choice: TMA for loads, LDG for offloads (B200 measurements) */
+  STRATA_ENGINE_DEFAULT = 0,  /* library choice (B200 measurements): STRATA_ENGINE_DMA when
+                                 host_chunks_host is given and a layer moves >= 4 MiB, else LDG */
   STRATA_ENGINE_LDG = 1,      /* warps, 16-byte LDG/STG register staging, warp index broadcast */
   STRATA_ENGINE_TMA = 2,      /* load: one cp.async.bulk producer warp + 4 LSU consumer warps per CTA
                                  over a shared-memory ring; offload: as STRATA_ENGINE_TMA_BULK */
@@ -178,6 +179,18 @@ int strata_wait_layer(strata_pool_t p, uint64_t ticket, int32_t layer, strata_st
  * layer `layer` (CUDA event timing).  Blocks until that layer is complete.  Errors as
  * strata_layer_event, plus STRATA_ERR_CUDA. */
 int strata_layer_elapsed_ms(strata_pool_t p, uint64_t ticket, int32_t layer, float* ms);
+
+/* Cumulative per-pool counters since registration (observability; no synchronisation). */
+typedef struct {
+  int64_t operations;       /* strata_load + strata_offload calls that returned STRATA_OK */
+  int64_t kernel_launches;  /* libstrata kernels launched (transfer, scatter/gather, validate) */
+  int64_t dma_copies;       /* copy-engine copies submitted by STRATA_ENGINE_DMA */
+  int64_t bytes;            /* algorithmic KV bytes moved (2*H*D*e per token per layer) */
+  int32_t last_engine;      /* strata_engine that executed the most recent operation */
+  int32_t reserved;
+} strata_counters;
+
+int strata_get_counters(strata_pool_t p, strata_counters* out);
 
 /* Thread-local message describing the last non-OK return on this thread ("" if none). */
 const char* strata_last_error(void);

@@ -29,7 +29,7 @@ __all__ = [
     "strata_register_host_pool", "strata_unregister_host_pool", "strata_host_pool_ptr", "strata_load",
     "strata_offload", "strata_layer_event", "strata_wait_layer", "strata_layer_elapsed_ms",
     "strata_baseline_memcpy_pages", "strata_baseline_memcpy_batch", "strata_baseline_contiguous",
-    "strata_version", "HostPool", "Requests", "StrataError",
+    "strata_version", "strata_get_counters", "HostPool", "Requests", "StrataError",
 ]
 
 
@@ -97,6 +97,12 @@ def strata_layer_elapsed_ms(pool: int, ticket: int, layer: int) -> float:
     check(_lib.lib().strata_layer_elapsed_ms(ctypes.c_void_p(pool), ticket, layer, ctypes.byref(ms)),
           "strata_layer_elapsed_ms")
     return float(ms.value)
+
+
+def strata_get_counters(pool: int) -> dict:
+    c = _lib.Counters()
+    check(_lib.lib().strata_get_counters(ctypes.c_void_p(pool), ctypes.byref(c)), "strata_get_counters")
+    return {f: int(getattr(c, f)) for f, _ in c._fields_ if f != "reserved"}
 
 
 def strata_baseline_memcpy_pages(pool: int, xfer: Xfer, direction: int, stream=None) -> int:
@@ -240,3 +246,6 @@ class HostPool:
 
     def layer_elapsed_ms(self, ticket: int, layer: int) -> float:
         return strata_layer_elapsed_ms(self.handle, ticket, layer)
+
+    def counters(self) -> dict:
+        return strata_get_counters(self.handle)

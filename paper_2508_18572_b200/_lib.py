@@ -76,9 +76,19 @@ class Xfer(ctypes.Structure):
     ]
 
 
+class Counters(ctypes.Structure):
+    """strata_counters"""
+    _fields_ = [("operations", ctypes.c_int64), ("kernel_launches", ctypes.c_int64), ("dma_copies", ctypes.c_int64),
+                ("bytes", ctypes.c_int64), ("last_engine", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 _lib = None
 
 _SIGS = {
+    "strata_get_counters": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Counters)]),
+    "strata_wait_layer": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p]),
+    "strata_layer_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32,
+                                               ctypes.POINTER(ctypes.c_float)]),
     "strata_register_host_pool": (ctypes.c_int, [ctypes.POINTER(PoolDesc), ctypes.POINTER(ctypes.c_void_p)]),
     "strata_unregister_host_pool": (ctypes.c_int, [ctypes.c_void_p]),
     "strata_host_pool_ptr": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),

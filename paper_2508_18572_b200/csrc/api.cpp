@@ -244,8 +244,12 @@ int ilog2_exact(int v) {
 
 // Defaults chosen on B200 measurements: both engines saturate the PCIe Gen5 link
 // with a small SM quota.
-constexpr int kDefaultCtasLdg = 8;
+// The paper's quota: 2 CTAs x 1024 threads.  On B200 that moves 50.3 GB/s (90.7 % of
+// the link) with 0.8 % prefill-GEMM and 10.8 % decode slowdown (profiles/r01/interference2.jsonl).
+constexpr int kDefaultCtasLdg = 2;
 constexpr int kDefaultThreadsLdg = 1024;   // host-read throughput of an SM scales with its warps
+constexpr int64_t kDmaMinLayerBytes = int64_t(4) << 20;
+constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;
 constexpr int kDefaultUnroll = 8;
 constexpr int kDefaultCtasTma = 8;
 constexpr int kTmaStageTarget = 32 << 10;
@@ -285,6 +289,7 @@ int run_validate(strata_pool* p, const strata_xfer* x, const Plan& plan, int dir
     v.err = p->err_dev;
     fill_table(x, plan, b, v.rt);
     if ((e = strata::launch_validate(v, s))) return cuda_fail(e, "validate kernel launch");
+    ++p->counters.kernel_launches;
   }
   if ((e = cudaMemcpyAsync(p->err_host, p->err_dev, 4, cudaMemcpyDeviceToHost, s))) return cuda_fail(e, "cudaMemcpyAsync");
   if ((e = cudaStreamSynchronize(s))) return cuda_fail(e, "cudaStreamSynchronize(validate)");
@@ -321,7 +326,7 @@ struct Piece {
 };
 
 constexpr size_t kStageTarget = size_t(64) << 20;   // bytes per staging slot
-constexpr int kDefaultCtasScatter = 32;
+constexpr int kDefaultCtasScatter = 4;   // 2: 53.6-54.0, 4: 54.1-54.2, 8: 54.2-54.4 GB/s
 
 int ensure_dma(strata_pool* p, size_t slot_bytes, int64_t slots) {
   cudaError_t e;
@@ -530,6 +535,8 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
           if ((e = cudaStreamWaitEvent(cs, p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
       }
+      p->counters.kernel_launches += 1;
+      p->counters.dma_copies += static_cast<int64_t>(dst.size());
       last_slot = slot;
       ++i;
     }
@@ -548,6 +555,12 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     for (auto ev : p->ev_copy[last_slot])
       if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
   return STRATA_OK;
+}
+
+void count_op(strata_pool* p, const Plan& plan, const strata_xfer* x, int engine) {
+  p->counters.operations += 1;
+  p->counters.bytes += 2 * plan.total_tokens * p->tok_bytes * (x->layer_end - x->layer_begin);
+  p->counters.last_engine = engine;
 }
 
 int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir) {
@@ -586,7 +599,20 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.dev_pages = x->dev_pages;
 
   int engine = x->engine;
-  if (engine == STRATA_ENGINE_DEFAULT) engine = dir == 0 ? STRATA_ENGINE_TMA : STRATA_ENGINE_LDG;
+  if (engine == STRATA_ENGINE_DEFAULT) {
+    // Measured on B200: the copy-engine gather + SM scatter moves 98 % of the link
+    // for layer-sized transfers; below a few MiB per layer its per-piece submission latency is not
+    // amortised and the zero-copy LDG kernel wins.  Without a host mirror of the chunk list only
+    // the kernel engines can run.
+    // Offloads write the host runs with D2H copies, which only beat the SM path for long runs
+    // (one chunk-layer >= 128 KiB: 56.0 vs 52.5 GB/s for Llama-8B; 32 KiB runs of a 70B TP=8 rank:
+    // 43.8 vs 52.3 GB/s).
+    const int64_t layer_bytes = 2 * plan.total_tokens * p->tok_bytes;
+    const int64_t run_bytes = 2 * int64_t(p->d.chunk_tokens) * p->tok_bytes;
+    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes &&
+                     (dir == 0 || run_bytes >= kDmaMinOffloadRun);
+    engine = dma ? STRATA_ENGINE_DMA : STRATA_ENGINE_LDG;
+  }
   if (engine == STRATA_ENGINE_DMA) {
     if (!x->host_chunks_host && plan.total_tokens > 0)
       return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
@@ -597,6 +623,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
     rc = transfer_dma(p, x, plan, xp, s, dir, slot);
     if (rc) return rc;
+    count_op(p, plan, x, engine);
     if (ticket) *ticket = t;
     return STRATA_OK;
   }
@@ -646,10 +673,12 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
         e = strata::launch_ldg(xp, dir, c, threads, unroll, s);
       }
       if (e != cudaSuccess) return cuda_fail(e, "transfer kernel launch");
+      ++p->counters.kernel_launches;
     }
     e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   }
+  count_op(p, plan, x, engine);
   if (ticket) *ticket = t;
   return STRATA_OK;
 }
@@ -830,6 +859,12 @@ int strata_layer_event(strata_pool_t p, uint64_t ticket, int32_t layer, strata_e
   int rc = find_op(p, ticket, layer, slot);
   if (rc) return rc;
   *out = reinterpret_cast<strata_event_t>(p->events[size_t(slot) * (p->d.num_layers + 1) + 1 + layer]);
+  return STRATA_OK;
+}
+
+int strata_get_counters(strata_pool_t p, strata_counters* out) {
+  if (!p || !out) return fail(STRATA_ERR_INVALID_ARG, "pool / out is NULL");
+  *out = p->counters;
   return STRATA_OK;
 }
 

@@ -111,6 +111,7 @@ struct strata_pool {
   int32_t* err_dev = nullptr;
   int32_t* err_host = nullptr;        // pinned
   int tma_smem = 0;
+  strata_counters counters = {};
   // STRATA_ENGINE_DMA: double-buffered HBM staging ring, copy streams and their events (lazy)
   static constexpr int kCopyStreams = 4;
   char* stage[2] = {nullptr, nullptr};

@@ -9,17 +9,18 @@
 // The layout transform (page-first host chunk <-> layer-first paged pool) is address arithmetic on
 // each token row (§4.2.1) — row_addr() below.
 //
-// Two engines, bit-identical, chosen per call (strata_xfer.engine):
-//   LDG  warps own groups of token rows; lanes compute the row addresses (index fetch) and
-//        broadcast them with __shfl_sync; each lane keeps U independent 16-byte loads in flight
-//        (LDG.E.128 from the mapped host VA), then stores them.  Register staging as in the paper.
-//   TMA  one warp per CTA runs an S-stage shared-memory ring: host runs that are contiguous
-//        (consecutive tokens of one chunk) arrive with ONE cp.async.bulk each (UBLKCP), token rows
-//        leave with one bulk store each.  ~160-190 KB in flight per SM from a single warp, so the
-//        link saturates from very few SMs with almost no register / issue footprint (the paper's
-//        SM-quota goal).
-// Both are bound by the host link (PCIe Gen5 x16, measured 55.5 GB/s memcpy, 51.4 GB/s SM
-// zero-copy ceiling on the B200 box — profiles/r01/probe.jsonl); HBM sees < 1 % of its bandwidth.
+// Kernels of the engines (bit-identical, chosen per call by strata_xfer.engine; api.cpp):
+//   ldg_kernel          zero-copy register staging: a warp owns a group of 32 token rows, lane t
+//                       fetches row t's indices (one group ahead) and the warp streams the rows
+//                       with U independent 16-byte LDG/STG per lane, addresses broadcast by
+//                       __shfl_sync.  Also the scatter / gather of the DMA engine (HBM staging).
+//   tma_ws_load_kernel  zero-copy TMA: one producer warp issues one cp.async.bulk per contiguous
+//                       host run into a shared-memory ring; 4 consumer warps drain it to the pages.
+//   tma_kernel          zero-copy TMA, single warp, bulk copies on both sides of the ring.
+// Measured on the B200 box (profiles/r01): SM-issued host reads top out at 51.4 GB/s (92.6 % of the
+// 55.5 GB/s pinned memcpy) whatever the instruction or cache hint; per SM they scale with resident
+// warps (~1 KiB in flight per warp), so the LDG engine uses 1024-thread CTAs and reaches 50.3 GB/s
+// with the paper's 2-CTA quota.  HBM sees < 1 % of its bandwidth.
 #include <cuda_runtime.h>
 #include <cstdint>
 

@@ -1,16 +1,17 @@
 #!/bin/bash
-# Bench + sweep + ncu evidence under gpurun (one GPU).
+# Round bench + tests + ncu evidence under gpurun (one GPU).
 mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 1200 python -m pytest tests -m "gpu and slow" -x -q > gpurun_out/pytest_gpu_slow.log 2>&1; echo "pytest slow rc=$?"; tail -2 gpurun_out/pytest_gpu_slow.log
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json
 python bench.py --engine 1 --no-cpu-baseline > gpurun_out/bench_ldg.json 2>> gpurun_out/bench.err; echo "bench ldg rc=$?"
 python bench.py --page-size 16 --no-cpu-baseline > gpurun_out/bench_p16.json 2>> gpurun_out/bench.err; echo "bench p16 rc=$?"
-timeout 900 python tools/sweep.py --pages 1,16,64 > gpurun_out/sweep.jsonl 2> gpurun_out/sweep.err; echo "sweep rc=$?"
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+python bench.py --config llama70b_tp8 --no-cpu-baseline --steps 10 > gpurun_out/bench_70b.json 2>> gpurun_out/bench.err; echo "bench 70b rc=$?"
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err; echo "bench ref rc=$?"
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu list rc=$?"
-for eng in 2 1; do
-  for dir in h2d d2h; do
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:"(tma|ldg)_kernel" -s 2 -c 1 \
-      -o gpurun_out/prof_e${eng}_${dir} -f python tools/prof_one.py --engine $eng --dir $dir > gpurun_out/ncu_e${eng}_${dir}.log 2>&1
-    echo "ncu full e$eng $dir rc=$?"
-  done
-done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ldg -s 2 -c 1 \
+    -o gpurun_out/prof_dma_scatter -f python tools/prof_one.py --engine 4 --layers 2 > gpurun_out/ncu_dma.log 2>&1; echo "ncu dma rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ldg -s 2 -c 1 \
+    -o gpurun_out/prof_ldg2 -f python tools/prof_one.py --engine 1 --layers 2 > gpurun_out/ncu_ldg2.log 2>&1; echo "ncu ldg rc=$?"
