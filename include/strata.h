@@ -66,7 +66,9 @@ enum strata_status {
   STRATA_ERR_CUDA = -5,         /* a CUDA runtime call failed (incl. an earlier async fault) */
   STRATA_ERR_OOM = -6,          /* host allocation / registration failed */
   STRATA_ERR_UNSUPPORTED = -7,  /* feature not available on this device / build */
-  STRATA_ERR_STALE_TICKET = -8  /* ticket older than the event ring, or not issued yet */
+  STRATA_ERR_STALE_TICKET = -8, /* ticket older than the event ring, or not issued yet */
+  STRATA_ERR_TIMEOUT = -9,      /* (strata_disk.h) job not settled within the timeout */
+  STRATA_ERR_IO = -10           /* (strata_disk.h) a file read / write failed */
 };
 
 enum strata_pool_flags {

@@ -23,6 +23,8 @@ STRATA_ERR_CUDA = -5
 STRATA_ERR_OOM = -6
 STRATA_ERR_UNSUPPORTED = -7
 STRATA_ERR_STALE_TICKET = -8
+STRATA_ERR_TIMEOUT = -9
+STRATA_ERR_IO = -10
 
 STRATA_HOST_HUGEPAGES = 1
 STRATA_HOST_WRITECOMBINED = 2
@@ -43,6 +45,7 @@ ERROR_NAMES = {
     0: "STRATA_OK", -1: "STRATA_ERR_INVALID_ARG", -2: "STRATA_ERR_ALIGNMENT",
     -3: "STRATA_ERR_INDEX_RANGE", -4: "STRATA_ERR_DUPLICATE", -5: "STRATA_ERR_CUDA",
     -6: "STRATA_ERR_OOM", -7: "STRATA_ERR_UNSUPPORTED", -8: "STRATA_ERR_STALE_TICKET",
+    -9: "STRATA_ERR_TIMEOUT", -10: "STRATA_ERR_IO",
 }
 
 

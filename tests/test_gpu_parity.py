@@ -355,15 +355,20 @@ def test_caller_owned_host_memory():
 # ------------------------------------------------------------------------------------------------
 # Full-size configs (BASELINE.json), in the launch configuration bench.py times.
 @pytest.mark.slow
-@pytest.mark.parametrize("P", [1, 16])
-def test_llama8b_32k_full(P):
+@pytest.mark.parametrize("P,engine", [(1, st.STRATA_ENGINE_DEFAULT), (16, st.STRATA_ENGINE_DEFAULT),
+                                      (1, st.STRATA_ENGINE_LDG)])
+def test_llama8b_32k_full(P, engine):
+    """Every byte of all 32 layers, in bench.py's launch configuration (default engine and quota:
+    the DMA engine) and with the zero-copy LDG engine at its default 2-CTA quota."""
     g = kvgen.geometry("llama8b_32k", P=P)
     q = kvgen.make_requests(kvgen.rng_for(0), [32768], g.P, g.C, g.num_pages, g.num_chunks)
     c = GpuCase(g, q)
     try:
-        c.pool.load(c.reqs)          # default engine + SM quota, as bench.py
+        c.pool.load(c.reqs, engine=engine)
         _sync()
         c.check_load(0, g.L)
+        used = c.pool.counters()["last_engine"]
+        assert used == (st.STRATA_ENGINE_DMA if engine == st.STRATA_ENGINE_DEFAULT else engine)
     finally:
         c.close()
 

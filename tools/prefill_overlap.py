@@ -25,6 +25,7 @@ import json
 import os
 import statistics
 import sys
+import threading
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -80,25 +81,37 @@ def main():
     if args.baseline and (g.P >= 16 or args.baseline > 1):   # 2M copies per load at P=1: seconds
         loaders["memcpy_pages_layerwise"] = -1
     layer_events = [ev() for _ in range(g.L)]
-    hx = reqs.xfer(0, g.L, host_lists=True)
 
     def issue_load(kind):
-        """Enqueue the whole load on `io`; returns a function giving layer l's completion event."""
+        """Enqueue the whole load on `io`; returns a function giving layer l's completion event.
+
+        The per-page baseline issues its copies from a loader thread (as a serving engine's cache
+        controller would), so the executor can enqueue layer l as soon as layer l's copies are
+        issued instead of after all 2*L*n/P of them."""
         if kind >= 0:
             t = pool.load(reqs, stream=io, engine=kind)
             return lambda l: ("strata", t, l)
-        for l in range(g.L):
-            hx.layer_begin, hx.layer_end = l, l + 1
-            st.strata_baseline_memcpy_pages(pool.handle, hx, st.STRATA_H2D, io)
-            layer_events[l].record(io)
-        return lambda l: ("event", layer_events[l], l)
+        issued = [threading.Event() for _ in range(g.L)]
+
+        def loader():
+            for l in range(g.L):
+                x = reqs.xfer(l, l + 1, host_lists=True)
+                st.strata_baseline_memcpy_pages(pool.handle, x, st.STRATA_H2D, io)
+                layer_events[l].record(io)
+                issued[l].set()
+        th = threading.Thread(target=loader)
+        th.start()
+        threads.append(th)
+        return lambda l: ("event", layer_events[l], l, issued[l])
 
     def wait(handle):
-        kind, a, l = handle
-        if kind == "strata":
-            pool.wait_layer(a, l, comp)
+        if handle[0] == "strata":
+            pool.wait_layer(handle[1], handle[2], comp)
         else:
-            comp.wait_event(a)
+            handle[3].wait()
+            comp.wait_event(handle[1])
+
+    threads = []
 
     for new in [int(x) for x in args.new.split(",")]:
         wrapper = flashinfer.BatchPrefillWithPagedKVCacheWrapper(ws, "NHD")
@@ -143,6 +156,8 @@ def main():
                 a, b, c = ev(), ev(), ev()
                 a.record(io)
                 issue_load(kind)
+                for th in threads:      # serial: every copy is issued before the end marker
+                    th.join()
                 b.record(io)
                 comp.wait_stream(io)
                 with torch.cuda.stream(comp):
@@ -150,6 +165,9 @@ def main():
                         layer(l)
                     c.record(comp)
                 c.synchronize()
+                for th in threads:
+                    th.join()
+                threads.clear()
                 serial.append(a.elapsed_time(c))
                 loadonly.append(a.elapsed_time(b))
                 # overlap: layer l's prefill waits only for layer l's load
@@ -164,6 +182,9 @@ def main():
                         layer(l)
                     c.record(comp)
                 c.synchronize()
+                for th in threads:
+                    th.join()
+                threads.clear()
                 overlap.append(a.elapsed_time(c))
             o = statistics.median(overlap)
             print(json.dumps({"cached": args.cached, "new": new, "load_compute_ratio": round(args.cached / new, 2),
