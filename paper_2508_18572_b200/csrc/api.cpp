@@ -391,9 +391,19 @@ cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::vector<v
   attr.dstLocHint.id = dir == 0 ? p->d.device : 0;
   const size_t n = dst.size();
   const int ns = strata_pool::kCopyStreams;
+  // cudaMemcpyBatchAsync refuses stream capture; under capture the copies become plain memcpy nodes
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaError_t e0 = cudaStreamIsCapturing(p->cs[0], &cap);
+  if (e0 != cudaSuccess) return e0;
+  const cudaMemcpyKind kind = dir == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
   for (int c = 0; c < ns; ++c) {
     const size_t lo = n * c / ns, hi = n * (c + 1) / ns;
-    if (hi > lo) {
+    if (hi > lo && cap == cudaStreamCaptureStatusActive) {
+      for (size_t i = lo; i < hi; ++i) {
+        cudaError_t e = cudaMemcpyAsync(dst[i], src[i], sz[i], kind, p->cs[c]);
+        if (e != cudaSuccess) return e;
+      }
+    } else if (hi > lo) {
       size_t idx = 0, fail_idx = 0;
       cudaError_t e = cudaMemcpyBatchAsync(dst.data() + lo, src.data() + lo, sz.data() + lo, hi - lo, &attr, &idx, 1,
                                            &fail_idx, p->cs[c]);
@@ -630,7 +640,9 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const bool tma = engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK;
   // TMA engine geometry: rows per stage (<= 32 lanes), stage bytes, depth
   if (tma) {
-    int rows = std::max(1, std::min(32, kTmaStageTarget / xp.tok_bytes));
+    // the warp-specialised ring is producer-bound per stage: larger stages (64 KiB) amortise it
+    const int target = engine == STRATA_ENGINE_TMA ? 2 * kTmaStageTarget : kTmaStageTarget;
+    int rows = std::max(1, std::min(32, target / xp.tok_bytes));
     const int sb = rows * xp.tok_bytes;
     const int budget = p->tma_smem - strata::tma_header_bytes(strata::kTmaMaxStages);
     int stages = std::min(strata::kTmaMaxStages, budget / sb);

@@ -331,7 +331,9 @@ __global__ void __launch_bounds__(32, 1) tma_kernel(const __grid_constant__ Xfer
 // unit only sees large contiguous host reads; the scattered small writes go through the LSU, so one
 // SM sustains ~45 GB/s of host reads and two saturate the PCIe link (the paper's 2-CTA quota,
 // PAPER.md:262).
-constexpr int kWsConsumers = 4;
+// Each consumer warp drains ~7 GB/s of st.global.v4 (tools/probe/tma_probe.cu ring_ws: 1/2/4/8
+// consumer warps -> 7/14/25/40 GB/s from one SM), so one SM needs ~8+ consumers to match the link.
+constexpr int kWsConsumers = 15;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
