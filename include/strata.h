@@ -83,7 +83,8 @@ enum strata_pool_flags {
 /* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
 enum strata_engine {
   STRATA_ENGINE_DEFAULT = 0,  /* library choice (B200 measurements): STRATA_ENGINE_DMA when
-                                 host_chunks_host is given and a layer moves >= 4 MiB, else LDG */
+                                 host_chunks_host is given and a layer moves >= 4 MiB (offloads then
+                                 group layers into >= 128 KiB runs, see layer_group), else LDG */
   STRATA_ENGINE_LDG = 1,      /* warps, 16-byte LDG/STG register staging, warp index broadcast */
   STRATA_ENGINE_TMA = 2,      /* load: one cp.async.bulk producer warp + 4 LSU consumer warps per CTA
                                  over a shared-memory ring; offload: as STRATA_ENGINE_TMA_BULK */
@@ -132,6 +133,11 @@ typedef struct {
   const int32_t* host_chunks_host;/* host mirror of host_chunks (same content), or NULL.  Required by
                                      STRATA_ENGINE_DMA (the CPU issues the copy-engine gathers);
                                      ignored by the kernel engines. */
+  int32_t layer_group;            /* STRATA_ENGINE_DMA: copy G consecutive layers of a chunk as one
+                                     run (page-first chunks keep them contiguous).  Layer l's event
+                                     then completes with its group [l0 + G*k, l0 + G*(k+1)), i.e.
+                                     coarser overlap for larger copies.  0 or 1 = per layer. */
+  int32_t reserved;
 } strata_xfer;
 
 /* Register the host tier and bind it to the device pool described by *d.

@@ -166,7 +166,7 @@ class Requests:
         return int(self.num_tokens.sum())
 
     def xfer(self, layer_begin: int, layer_end: int, engine: int = 0, num_ctas: int = 0, threads: int = 0,
-             host_lists: bool = False) -> Xfer:
+             host_lists: bool = False, layer_group: int = 0) -> Xfer:
         """strata_xfer pointing at these tables (device lists, or host lists for the baselines)."""
         hc = self.host_chunks_h.ctypes.data if host_lists else self.host_chunks_d.data_ptr()
         dp = self.dev_pages_h.ctypes.data if host_lists else self.dev_pages_d.data_ptr()
@@ -175,7 +175,8 @@ class Requests:
                     host_chunks=hc, chunk_start=self.chunk_start.ctypes.data, dev_pages=dp,
                     page_start=self.page_start.ctypes.data, chunk_offset=self.chunk_offset.ctypes.data,
                     page_offset=self.page_offset.ctypes.data, host_chunks_len=self.host_chunks_h.size,
-                    dev_pages_len=self.dev_pages_h.size, host_chunks_host=self.host_chunks_h.ctypes.data)
+                    dev_pages_len=self.dev_pages_h.size, host_chunks_host=self.host_chunks_h.ctypes.data,
+                    layer_group=layer_group)
 
 
 class HostPool:
@@ -229,13 +230,15 @@ class HostPool:
             pass
 
     def load(self, reqs: Requests, layer_begin: int = 0, layer_end: Optional[int] = None, stream=None,
-             engine: int = 0, num_ctas: int = 0, threads: int = 0) -> int:
-        x = reqs.xfer(layer_begin, self.num_layers if layer_end is None else layer_end, engine, num_ctas, threads)
+             engine: int = 0, num_ctas: int = 0, threads: int = 0, layer_group: int = 0) -> int:
+        x = reqs.xfer(layer_begin, self.num_layers if layer_end is None else layer_end, engine, num_ctas, threads,
+                      layer_group=layer_group)
         return strata_load(self.handle, x, stream)
 
     def offload(self, reqs: Requests, layer_begin: int = 0, layer_end: Optional[int] = None, stream=None,
-                engine: int = 0, num_ctas: int = 0, threads: int = 0) -> int:
-        x = reqs.xfer(layer_begin, self.num_layers if layer_end is None else layer_end, engine, num_ctas, threads)
+                engine: int = 0, num_ctas: int = 0, threads: int = 0, layer_group: int = 0) -> int:
+        x = reqs.xfer(layer_begin, self.num_layers if layer_end is None else layer_end, engine, num_ctas, threads,
+                      layer_group=layer_group)
         return strata_offload(self.handle, x, stream)
 
     def layer_event(self, ticket: int, layer: int) -> int:

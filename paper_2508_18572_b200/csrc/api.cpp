@@ -175,6 +175,7 @@ int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan) {
   if (x->num_reqs < 0) return fail(STRATA_ERR_INVALID_ARG, "num_reqs < 0");
   if (x->engine < 0 || x->engine > STRATA_ENGINE_DMA) return fail(STRATA_ERR_INVALID_ARG, "unknown engine %d", x->engine);
   if (x->num_ctas < 0 || x->num_ctas > 65535) return fail(STRATA_ERR_INVALID_ARG, "num_ctas out of range");
+  if (x->layer_group < 0) return fail(STRATA_ERR_INVALID_ARG, "layer_group < 0");
   if (x->threads < 0 || x->threads > 1024 || x->threads % 32)
     return fail(STRATA_ERR_INVALID_ARG, "threads must be a multiple of 32 in [32,1024]");
   if (x->num_reqs == 0) return STRATA_OK;
@@ -251,7 +252,7 @@ constexpr int kDefaultThreadsLdg = 1024;   // host-read throughput of an SM scal
 constexpr int64_t kDmaMinLayerBytes = int64_t(4) << 20;
 constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;
 constexpr int kDefaultUnroll = 8;
-constexpr int kDefaultCtasTma = 8;
+constexpr int kDefaultCtasTma = 2;   // warp-specialised ring: 51.0 GB/s at 2 CTAs (sweep_tma_ws15.jsonl)
 constexpr int kTmaStageTarget = 32 << 10;
 
 int run_validate(strata_pool* p, const strata_xfer* x, const Plan& plan, int dir, cudaStream_t s) {
@@ -436,7 +437,15 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     }
   }
   const size_t unit = static_cast<size_t>(2 * C * tok);             // one chunk-layer: K rows, V rows
-  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), kStageTarget / unit));
+  // layers per copy run.  Loads keep per-layer granularity (grouping does not raise H2D throughput,
+  // profiles/r01/sweep_groups*.jsonl); offloads ("backup", a non-critical path) group
+  // layers until a run is >= 128 KiB, which D2H copies need (70B TP=8 rank: 44.6 -> 55.8 GB/s).
+  int G = x->layer_group;
+  if (G <= 0)
+    G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + 2 * C * tok - 1) / (2 * C * tok)));
+  G = std::max(1, G);
+  const size_t gunit = unit * static_cast<size_t>(G);                 // staging bytes per chunk
+  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), kStageTarget / gunit));
   // pieces: <= per_piece chunk positions and <= kMaxReqsPerLaunch requests each
   std::vector<Piece> pieces;
   for (size_t k = 0; k < pos.size();) {
@@ -454,7 +463,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     }
     pieces.push_back(pc);
   }
-  int rc = ensure_dma(p, per_piece * unit, static_cast<int64_t>(per_piece));
+  int rc = ensure_dma(p, per_piece * gunit, static_cast<int64_t>(per_piece));
   if (rc) return rc;
 
   cudaError_t e;
@@ -462,8 +471,8 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;
   xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows
   const int ctas = x->num_ctas ? x->num_ctas : kDefaultCtasScatter;
-  xp.chunk_bytes = static_cast<int64_t>(unit);
-  xp.layer_off = 0;
+  // staging slot j holds chunk position j's G layers: [G][K,V][C][H][D], a compact host tier
+  xp.chunk_bytes = static_cast<int64_t>(gunit);
   xp.kv_off = C * tok;
   xp.host_chunks = p->slot_ids;
 
@@ -474,31 +483,34 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   std::vector<size_t> sz;
   int64_t i = 0;
   int last_slot = 0;
-  for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
-    xp.kbase = static_cast<char*>(p->k[l]);
-    xp.vbase = static_cast<char*>(p->v[l]);
+  auto layer_event = [&](int32_t l) { return p->events[size_t(slot_ev) * (L + 1) + 1 + l]; };
+  for (int32_t lg = x->layer_begin; lg < x->layer_end; lg += G) {
+    const int gl = std::min<int>(G, x->layer_end - lg);   // layers in this group
     for (const Piece& pc : pieces) {
+      const bool last_piece = &pc == &pieces.back();
       const int slot = static_cast<int>(i & 1);
       char* stage = p->stage[slot];
-      // copy list of this piece for layer l (host <-> staging slot)
+      // copy list of this piece for layers [lg, lg+gl) (host <-> staging slot)
       dst.clear();
       src.clear();
       sz.clear();
       for (size_t j = 0; j < pc.count; ++j) {
         const ChunkPos& cp = pos[pc.first + j];
         const int64_t hc = x->host_chunks_host[x->chunk_start[cp.req] + cp.cq];
-        char* h = p->host + hc * p->chunk_bytes + int64_t(l) * 2 * C * tok;
-        char* d = stage + j * unit;
+        char* h = p->host + hc * p->chunk_bytes + int64_t(lg) * 2 * C * tok;
+        char* d = stage + j * gunit;
         auto add = [&](int64_t off, int64_t bytes) {
           dst.push_back(dir == 0 ? d + off : h + off);
           src.push_back(dir == 0 ? h + off : d + off);
           sz.push_back(static_cast<size_t>(bytes));
         };
         if (cp.lo == 0 && cp.cnt == C) {
-          add(0, 2 * C * tok);                         // K and V runs are adjacent: one copy
+          add(0, gl * 2 * C * tok);                    // the group's K,V runs are adjacent: one copy
         } else {
-          add(cp.lo * tok, cp.cnt * tok);              // K rows
-          add((C + cp.lo) * tok, cp.cnt * tok);        // V rows
+          for (int g = 0; g < gl; ++g) {
+            add(g * 2 * C * tok + cp.lo * tok, cp.cnt * tok);        // K rows of layer lg+g
+            add(g * 2 * C * tok + (C + cp.lo) * tok, cp.cnt * tok);  // V rows
+          }
         }
       }
       // request table of the piece: sub-requests addressing staging slots
@@ -524,42 +536,57 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
       xp.host = stage;
       const int64_t groups = (2LL * acc + xp.rows_per_group - 1) / xp.rows_per_group;
       const int c = static_cast<int>(std::min<int64_t>(ctas, (groups * 32 + threads - 1) / threads));
+      // one scatter / gather launch per layer of the group over the slot's layer sub-blocks
+      auto launch_group = [&](int kdir) -> cudaError_t {
+        for (int g = 0; g < gl; ++g) {
+          xp.kbase = static_cast<char*>(p->k[lg + g]);
+          xp.vbase = static_cast<char*>(p->v[lg + g]);
+          xp.layer_off = int64_t(g) * 2 * C * tok;
+          cudaError_t le = strata::launch_ldg(xp, kdir, c, threads, unroll, s);
+          if (le != cudaSuccess) return le;
+          ++p->counters.kernel_launches;
+          // loads: layer lg+g is complete once its scatter of the group's last piece has run
+          if (kdir == 0 && last_piece && (le = cudaEventRecord(layer_event(lg + g), s))) return le;
+        }
+        return cudaSuccess;
+      };
       if (dir == 0) {
-        // copies into the slot (after its previous scatter), then the scatter on the caller's stream
+        // copies into the slot (after its previous scatter), then the scatters on the caller's stream
         if (i >= 2)
           for (auto cs : p->cs)
             if ((e = cudaStreamWaitEvent(cs, p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
         for (auto ev : p->ev_copy[slot])
           if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = strata::launch_ldg(xp, 0, c, threads, unroll, s))) return cuda_fail(e, "scatter kernel launch");
+        if ((e = launch_group(0))) return cuda_fail(e, "scatter kernel launch");
         if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
       } else {
-        // gather into the slot (after its previous copies drained), then copies to the host tier
+        // gathers into the slot (after its previous copies drained), then copies to the host tier
         if (i >= 2)
           for (auto ev : p->ev_copy[slot])
             if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = strata::launch_ldg(xp, 1, c, threads, unroll, s))) return cuda_fail(e, "gather kernel launch");
+        if ((e = launch_group(1))) return cuda_fail(e, "gather kernel launch");
         if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
         for (auto cs : p->cs)
           if ((e = cudaStreamWaitEvent(cs, p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
       }
-      p->counters.kernel_launches += 1;
       p->counters.dma_copies += static_cast<int64_t>(dst.size());
       last_slot = slot;
       ++i;
     }
-    cudaEvent_t lev = p->events[size_t(slot_ev) * (L + 1) + 1 + l];
-    if (dir == 0) {
-      e = cudaEventRecord(lev, s);
-    } else {
-      // host bytes of layer l are written once every copy stream has passed the layer's last piece
-      for (int c = 1; c < strata_pool::kCopyStreams; ++c)
-        if ((e = cudaStreamWaitEvent(p->cs[0], p->ev_copy[last_slot][c], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-      e = cudaEventRecord(lev, p->cs[0]);
+    if (dir == 0 && pieces.empty()) {
+      for (int g = 0; g < gl; ++g)
+        if ((e = cudaEventRecord(layer_event(lg + g), s))) return cuda_fail(e, "cudaEventRecord");
+    } else if (dir == 1) {
+      // host bytes of the group are written once every copy stream has passed its last piece
+      if (!pieces.empty())
+        for (int c = 1; c < strata_pool::kCopyStreams; ++c)
+          if ((e = cudaStreamWaitEvent(p->cs[0], p->ev_copy[last_slot][c], 0)))
+            return cuda_fail(e, "cudaStreamWaitEvent");
+      for (int g = 0; g < gl; ++g)
+        if ((e = cudaEventRecord(layer_event(lg + g), p->cs[0]))) return cuda_fail(e, "cudaEventRecord");
     }
-    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
   }
   if (dir == 1 && i > 0)  // join: the caller's stream is ordered after every copy
     for (auto ev : p->ev_copy[last_slot])
@@ -614,13 +641,9 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     // for layer-sized transfers; below a few MiB per layer its per-piece submission latency is not
     // amortised and the zero-copy LDG kernel wins.  Without a host mirror of the chunk list only
     // the kernel engines can run.
-    // Offloads write the host runs with D2H copies, which only beat the SM path for long runs
-    // (one chunk-layer >= 128 KiB: 56.0 vs 52.5 GB/s for Llama-8B; 32 KiB runs of a 70B TP=8 rank:
-    // 43.8 vs 52.3 GB/s).
+    // (Offloads group layers into >= 128 KiB runs inside the DMA engine, see transfer_dma.)
     const int64_t layer_bytes = 2 * plan.total_tokens * p->tok_bytes;
-    const int64_t run_bytes = 2 * int64_t(p->d.chunk_tokens) * p->tok_bytes;
-    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes &&
-                     (dir == 0 || run_bytes >= kDmaMinOffloadRun);
+    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes;
     engine = dma ? STRATA_ENGINE_DMA : STRATA_ENGINE_LDG;
   }
   if (engine == STRATA_ENGINE_DMA) {

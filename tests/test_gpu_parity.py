@@ -154,21 +154,25 @@ def test_special_float_payloads(engine):
 
 
 @pytest.mark.parametrize("direction", ["load", "offload"])
-def test_dma_engine_multi_piece(direction):
+@pytest.mark.parametrize("group", [1, 2, 4])
+def test_dma_engine_multi_piece(direction, group):
     """STRATA_ENGINE_DMA with layers larger than one 64 MiB staging slot: several pieces per layer
-    alternate between the two slots, within and across layers; partial first/last chunks."""
+    alternate between the two slots, within and across layers; partial first/last chunks; layer
+    groups (G layers of a chunk per copy, ragged last group)."""
     g = Geometry(6, 8, 128, 2, 1, 64, 40960, 560)
     rng = kvgen.rng_for(21)
     q = kvgen.make_requests(rng, [20000, 13000, 77], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
     c = GpuCase(g, q, dev_fill="canary" if direction == "load" else "random")
     try:
         if direction == "load":
-            c.pool.load(c.reqs, 1, 6, engine=st.STRATA_ENGINE_DMA)
+            t = c.pool.load(c.reqs, 1, 6, engine=st.STRATA_ENGINE_DMA, layer_group=group)
             _sync()
             c.check_load(1, 6)
+            done = [c.pool.layer_elapsed_ms(t, l) for l in range(1, 6)]
+            assert all(b >= a for a, b in zip(done, done[1:])), done
         else:
             before = c.pool.host.copy()
-            c.pool.offload(c.reqs, 0, 5, engine=st.STRATA_ENGINE_DMA)
+            c.pool.offload(c.reqs, 0, 5, engine=st.STRATA_ENGINE_DMA, layer_group=group)
             _sync()
             assert np.array_equal(c.pool.host, c.expected_offload(before, 0, 5))
     finally:

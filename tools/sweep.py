@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--flags", type=int, default=0, help="strata_pool_desc.flags (host allocation)")
     ap.add_argument("--tag", default="")
     ap.add_argument("--threads", type=int, default=0, help="LDG engine threads per CTA (0 = default)")
+    ap.add_argument("--groups", default="0", help="DMA layer_group values to sweep")
     args = ap.parse_args()
     io = torch.cuda.Stream()
     for P in [int(x) for x in args.pages.split(",")]:
@@ -75,10 +76,13 @@ def main():
         base = {"config": args.config, "P": P, "L": g.L, "tokens": q.total_tokens, "bytes": nbytes, "frag": args.frag,
                 "chunk_frag": args.chunk_frag, "flags": args.flags, "tag": args.tag}
         for eng in [int(x) for x in args.engines.split(",")]:
+          for G in ([int(x) for x in args.groups.split(",")] if eng == 4 else [0]):
             for c in [int(x) for x in args.ctas.split(",")]:
                 for d, fn in (("h2d", pool.load), ("d2h", pool.offload)):
-                    ev, wall = timed(lambda: fn(reqs, stream=io, engine=eng, num_ctas=c, threads=args.threads), io)
+                    ev, wall = timed(lambda: fn(reqs, stream=io, engine=eng, num_ctas=c, threads=args.threads,
+                                                layer_group=G), io)
                     print(json.dumps({**base, "method": "strata", "dir": d, "engine": eng, "ctas": c, "threads": args.threads,
+                                      "layer_group": G,
                                       "ms": round(ev * 1e3, 3), "wall_ms": round(wall * 1e3, 3),
                                       "gbs": round(nbytes / ev / 1e9, 3)}), flush=True)
         if args.baselines == "1":
