@@ -92,6 +92,43 @@ def test_cancel_credits_finished_chunks(tmp_path):
                 assert not chunk.any(), "a cancelled chunk must not be written"
 
 
+@pytest.mark.gpu
+def test_disk_to_host_to_gpu(tmp_path):
+    """The three tiers end to end: host chunks written back to disk, prefetched into a registered
+    host tier at other positions, then strata_load'ed into the paged pool — bit-exact vs the oracle
+    loading the original host bytes."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import oracle
+    from tests.gpu_helpers import GpuCase
+    g = kvgen.Geometry(4, 2, 64, 2, 4, 16, 256, 40)
+    q = kvgen.make_requests(kvgen.rng_for(5), [300, 97], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
+    src = kvgen.random_bytes(kvgen.rng_for(6), g.host_bytes)       # the "original" host tier
+    c = GpuCase(g, q, host_fill="none")
+    try:
+        c.pool.host[:] = 0
+        cb = g.chunk_bytes
+        with sd.DiskTier(str(tmp_path / "tier.bin"), cb, g.L, 64, io_threads=4) as tier:
+            staging = sd.aligned_empty(g.host_bytes)
+            staging[:] = src
+            used = sorted(set(q.host_chunks.tolist()))
+            disk_ids = [60 - i for i in range(len(used))]
+            assert tier.wait(tier.writeback(staging, used, disk_ids))[0] == 0
+            assert tier.wait(tier.prefetch(c.pool.host, disk_ids, used))[0] == 0
+        c.pool.load(c.reqs)
+        torch.cuda.synchronize()
+        for l in range(g.L):
+            ek, ev = [None] * g.L, [None] * g.L
+            ek[l] = np.full(c.layer_bytes, 0xA5, np.uint8)
+            ev[l] = np.full(c.layer_bytes, 0xA5, np.uint8)
+            oracle.load(g, src, ek, ev, q, l, l + 1)
+            assert np.array_equal(c.k[l].cpu().numpy(), ek[l])
+            assert np.array_equal(c.v[l].cpu().numpy(), ev[l])
+    finally:
+        c.close()
+
+
 def test_errors(tmp_path):
     path = str(tmp_path / "t.bin")
     with pytest.raises(_lib.StrataError) as e:
