@@ -33,6 +33,7 @@ import kvgen  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 ENGINE_NAMES = {0: "default", 1: "ldg", 2: "tma", 3: "tma_bulk", 4: "dma"}
+SM_ZERO_COPY_CEILING = 51.44   # GB/s, profiles/r01/probe.jsonl: SM-issued host reads, best of the sweep
 PATH_DESC = {
     "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (cudaMemcpyBatchAsync, 4 streams) "
            "into an HBM staging slot + ldg_kernel scatter to the pages; one event per layer",
@@ -323,9 +324,20 @@ def main():
 
     out = None
     if rank == 0:
+        # per layer (= per launch for the kernel engines; per copy+scatter group for DMA): the median
+        # timed step divided over its layers, from CUDA events on the I/O stream
         per_launch_bytes = bytes_step // g.L
-        avg_launch = statistics.mean(launch_ms[1:]) if len(launch_ms) > 1 else launch_ms[0]
+        avg_launch = step_stats["median_ms"] / g.L
         achieved = per_launch_bytes / (avg_launch / 1e3) / 1e9
+        # the hand-written zero-copy kernels against both ceilings: the link, and the SM-issued
+        # zero-copy read plateau measured by tools/probe/probe.cu on this pool (51.44 GB/s)
+        zc = {}
+        for name in ("ldg", "tma"):
+            gbs = others.get(name) if name != engine_used else round(value / world, 3)
+            if gbs is not None:
+                zc[name] = {"value": gbs, "frac_of_link": round(gbs / link_peak, 4),
+                            "frac_of_sm_zero_copy_ceiling": round(gbs / SM_ZERO_COPY_CEILING, 4),
+                            "num_ctas": "default (2 x 1024 threads)" if name == "ldg" else "default (2 x 512 threads)"}
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
@@ -364,6 +376,8 @@ def main():
             "clocks": clocks.summary(),
             "engine": engine_used, "num_ctas": args.num_ctas or "default",
             "other_engines_gbs": others,
+            "zero_copy_kernels": zc,
+            "per_layer_ms_last_step": [round(x, 4) for x in launch_ms],
         }
         print(json.dumps(out), flush=True)
     pool.close()
