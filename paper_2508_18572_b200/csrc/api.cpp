@@ -332,6 +332,8 @@ constexpr int kDefaultCtasScatter = 4;   // 2: 53.6-54.0, 4: 54.1-54.2, 8: 54.2-
 int ensure_dma(strata_pool* p, size_t slot_bytes, int64_t slots) {
   cudaError_t e;
   if (!p->cs[0]) {
+    if (const char* v = getenv("STRATA_COPY_STREAMS"))
+      p->ncs = std::max(1, std::min(strata_pool::kCopyStreams, atoi(v)));
     for (auto& c : p->cs)
       if ((e = cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking))) return cuda_fail(e, "cudaStreamCreate");
     if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
@@ -391,7 +393,7 @@ cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::vector<v
   attr.dstLocHint.type = dir == 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
   attr.dstLocHint.id = dir == 0 ? p->d.device : 0;
   const size_t n = dst.size();
-  const int ns = strata_pool::kCopyStreams;
+  const int ns = p->ncs;
   // cudaMemcpyBatchAsync refuses stream capture; under capture the copies become plain memcpy nodes
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaError_t e0 = cudaStreamIsCapturing(p->cs[0], &cap);
@@ -477,8 +479,8 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   xp.host_chunks = p->slot_ids;
 
   if ((e = cudaEventRecord(p->ev_fork, s))) return cuda_fail(e, "cudaEventRecord");
-  for (auto c : p->cs)
-    if ((e = cudaStreamWaitEvent(c, p->ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+  for (int ci = 0; ci < p->ncs; ++ci)
+    if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
   std::vector<void*> dst, src;
   std::vector<size_t> sz;
   int64_t i = 0;
@@ -550,25 +552,26 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
         }
         return cudaSuccess;
       };
+      const int ncs = p->ncs;
       if (dir == 0) {
         // copies into the slot (after its previous scatter), then the scatters on the caller's stream
         if (i >= 2)
-          for (auto cs : p->cs)
-            if ((e = cudaStreamWaitEvent(cs, p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+          for (int ci = 0; ci < ncs; ++ci)
+            if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
-        for (auto ev : p->ev_copy[slot])
-          if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        for (int ci = 0; ci < ncs; ++ci)
+          if ((e = cudaStreamWaitEvent(s, p->ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = launch_group(0))) return cuda_fail(e, "scatter kernel launch");
         if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
       } else {
         // gathers into the slot (after its previous copies drained), then copies to the host tier
         if (i >= 2)
-          for (auto ev : p->ev_copy[slot])
-            if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+          for (int ci = 0; ci < ncs; ++ci)
+            if ((e = cudaStreamWaitEvent(s, p->ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = launch_group(1))) return cuda_fail(e, "gather kernel launch");
         if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
-        for (auto cs : p->cs)
-          if ((e = cudaStreamWaitEvent(cs, p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        for (int ci = 0; ci < ncs; ++ci)
+          if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
       }
       p->counters.dma_copies += static_cast<int64_t>(dst.size());
@@ -581,7 +584,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     } else if (dir == 1) {
       // host bytes of the group are written once every copy stream has passed its last piece
       if (!pieces.empty())
-        for (int c = 1; c < strata_pool::kCopyStreams; ++c)
+        for (int c = 1; c < p->ncs; ++c)
           if ((e = cudaStreamWaitEvent(p->cs[0], p->ev_copy[last_slot][c], 0)))
             return cuda_fail(e, "cudaStreamWaitEvent");
       for (int g = 0; g < gl; ++g)
@@ -589,8 +592,8 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     }
   }
   if (dir == 1 && i > 0)  // join: the caller's stream is ordered after every copy
-    for (auto ev : p->ev_copy[last_slot])
-      if ((e = cudaStreamWaitEvent(s, ev, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+    for (int ci = 0; ci < p->ncs; ++ci)
+      if ((e = cudaStreamWaitEvent(s, p->ev_copy[last_slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
   return STRATA_OK;
 }
 

@@ -113,7 +113,8 @@ struct strata_pool {
   int tma_smem = 0;
   strata_counters counters = {};
   // STRATA_ENGINE_DMA: double-buffered HBM staging ring, copy streams and their events (lazy)
-  static constexpr int kCopyStreams = 4;
+  static constexpr int kCopyStreams = 8;  // capacity; `ncs` are used (env STRATA_COPY_STREAMS, default 4)
+  int ncs = 4;
   char* stage[2] = {nullptr, nullptr};
   size_t stage_bytes = 0;             // bytes per staging slot
   int32_t* slot_ids = nullptr;        // device iota [0, slot_cap): chunk index of each staging slot

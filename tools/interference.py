@@ -73,6 +73,8 @@ def main():
     ap.add_argument("--ctas", default="1,2,4,8,16")
     ap.add_argument("--engines", default="1,2")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--groups", default="0", help="DMA layer_group values (engine 4 only)")
+    ap.add_argument("--memcpy", type=int, default=0, help="also co-run a contiguous cudaMemcpyAsync loop (-1 engine)")
     args = ap.parse_args()
 
     g = kvgen.geometry("llama8b_32k")
@@ -91,14 +93,32 @@ def main():
     alone = {name: time_proxy(fn, comp, args.reps) for name, fn in proxies.items()}
     print(json.dumps({"kind": "proxy_alone", **{k_: round(v_, 4) for k_, v_ in alone.items()}}), flush=True)
 
+    scratch = torch.empty(bytes_load // g.L, dtype=torch.uint8, device="cuda")
+
+    def make_io(eng, c, G):
+        if eng < 0:   # contiguous memcpy of the same bytes: 32 copies of one layer's worth
+            def run():
+                for _ in range(g.L):
+                    st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, scratch.numel(), io)
+            return run
+        return lambda: pool.load(reqs, stream=io, engine=eng, num_ctas=c, layer_group=G)
+
+    configs = []
     for eng in [int(x) for x in args.engines.split(",")]:
         for c in [int(x) for x in args.ctas.split(",")]:
+            for G in ([int(x) for x in args.groups.split(",")] if eng == 4 else [0]):
+                configs.append((eng, c, G))
+    if args.memcpy:
+        configs.append((-1, 0, 0))
+    for eng, c, G in configs:
+        if True:
+            load = make_io(eng, c, G)
             # I/O alone
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            pool.load(reqs, stream=io, engine=eng, num_ctas=c)
+            load()
             a.record(io)
             for _ in range(3):
-                pool.load(reqs, stream=io, engine=eng, num_ctas=c)
+                load()
             b.record(io)
             b.synchronize()
             io_alone = 3 * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
@@ -109,12 +129,12 @@ def main():
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(io)
                 for _ in range(n_loads):
-                    pool.load(reqs, stream=io, engine=eng, num_ctas=c)
+                    load()
                 b.record(io)
                 t_co = time_proxy(fn, comp, args.reps)
                 b.synchronize()
                 io_co = n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
-                print(json.dumps({"kind": "corun", "engine": eng, "ctas": c, "proxy": name,
+                print(json.dumps({"kind": "corun", "engine": eng, "ctas": c, "layer_group": G, "proxy": name,
                                   "proxy_alone_ms": round(alone[name], 4), "proxy_corun_ms": round(t_co, 4),
                                   "slowdown": round(t_co / alone[name] - 1, 4), "io_alone_gbs": round(io_alone, 2),
                                   "io_corun_gbs_upper": round(io_co, 2)}), flush=True)
