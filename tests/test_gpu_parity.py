@@ -63,8 +63,9 @@ def _fuzz_params(i):
     engine = ENGINES[i % len(ENGINES)]
     frag = "churn" if rng.random() < 0.3 else "perm"
     layout = rng.choice(["nhd", "hnd", "padded"])
+    group = int(rng.choice([0, 1, 2, 3])) if engine == st.STRATA_ENGINE_DMA else 0
     return dict(rng=rng, L=L, H=H, D=D, e=e, P=P, C=C, ns=ns, l0=l0, l1=l1, ctas=ctas, engine=engine,
-                frag=frag, layout=str(layout))
+                frag=frag, layout=str(layout), group=group)
 
 
 def _fuzz_case(i):
@@ -95,7 +96,7 @@ def test_fuzz_load(i):
     f, g, q, strides = _fuzz_case(i)
     c = GpuCase(g, q, strides=strides, seed=i)
     try:
-        c.pool.load(c.reqs, f["l0"], f["l1"], engine=f["engine"], num_ctas=f["ctas"])
+        c.pool.load(c.reqs, f["l0"], f["l1"], engine=f["engine"], num_ctas=f["ctas"], layer_group=f["group"])
         _sync()
         c.check_load(f["l0"], f["l1"])
     finally:
@@ -108,7 +109,7 @@ def test_fuzz_offload(i):
     c = GpuCase(g, q, strides=strides, seed=i, dev_fill="random")
     try:
         before = c.pool.host.copy()
-        c.pool.offload(c.reqs, f["l0"], f["l1"], engine=f["engine"], num_ctas=f["ctas"])
+        c.pool.offload(c.reqs, f["l0"], f["l1"], engine=f["engine"], num_ctas=f["ctas"], layer_group=f["group"])
         _sync()
         exp = c.expected_offload(before, f["l0"], f["l1"])
         got = c.pool.host
