@@ -420,7 +420,8 @@ cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::vector<v
 
 int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata::XferParams xp, cudaStream_t s,
                  int dir, int slot_ev) {
-  if (!x->host_chunks_host) return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
+  if (!x->host_chunks_host && plan.total_tokens > 0)
+    return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
   const int64_t C = p->d.chunk_tokens, P = p->d.page_size, tok = p->tok_bytes;
   const int L = p->d.num_layers;
   // chunk positions of the call, request by request
@@ -445,7 +446,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   int G = x->layer_group;
   if (G <= 0)
     G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + 2 * C * tok - 1) / (2 * C * tok)));
-  G = std::max(1, G);
+  G = std::max(1, std::min(G, std::max(1, x->layer_end - x->layer_begin)));
   const size_t gunit = unit * static_cast<size_t>(G);                 // staging bytes per chunk
   const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), kStageTarget / gunit));
   // pieces: <= per_piece chunk positions and <= kMaxReqsPerLaunch requests each
@@ -656,9 +657,15 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     const int slot = static_cast<int>(t % kEventRing);
     p->ops[slot] = {t, x->layer_begin, x->layer_end};
     e = cudaEventRecord(p->events[size_t(slot) * (p->d.num_layers + 1)], s);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    if (e != cudaSuccess) {
+      p->ops[slot].ticket = 0;   // a failed operation has no valid events
+      return cuda_fail(e, "cudaEventRecord");
+    }
     rc = transfer_dma(p, x, plan, xp, s, dir, slot);
-    if (rc) return rc;
+    if (rc) {
+      p->ops[slot].ticket = 0;
+      return rc;
+    }
     count_op(p, plan, x, engine);
     if (ticket) *ticket = t;
     return STRATA_OK;
@@ -693,8 +700,13 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const int slot = static_cast<int>(t % kEventRing);
   p->ops[slot] = {t, x->layer_begin, x->layer_end};
   const int L = p->d.num_layers;
+  // a failed operation keeps no ticket: its ring slot must not hand out stale events
+  auto op_fail = [&](cudaError_t err, const char* what) {
+    p->ops[slot].ticket = 0;
+    return cuda_fail(err, what);
+  };
   e = cudaEventRecord(p->events[size_t(slot) * (L + 1)], s);  // operation start
-  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+  if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
   for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
     xp.kbase = static_cast<char*>(p->k[l]);
     xp.vbase = static_cast<char*>(p->v[l]);
@@ -714,11 +726,11 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
         if (need < c) c = static_cast<int>(need);
         e = strata::launch_ldg(xp, dir, c, threads, unroll, s);
       }
-      if (e != cudaSuccess) return cuda_fail(e, "transfer kernel launch");
+      if (e != cudaSuccess) return op_fail(e, "transfer kernel launch");
       ++p->counters.kernel_launches;
     }
     e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], s);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
   }
   count_op(p, plan, x, engine);
   if (ticket) *ticket = t;
