@@ -1,0 +1,308 @@
+// dma.cpp — STRATA_ENGINE_DMA (include/strata.h): copy engines gather whole page-first runs into an
+// HBM staging ring, the LDG kernel scatters them to the pages (offload: the mirror).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace strata {
+
+// -------------------------------------------------------------------------------------------------
+// STRATA_ENGINE_DMA: copy engines move whole page-first runs, an SM kernel does the scatter.
+//
+// The page-first host tier keeps, for one layer, the K rows and then the V rows of a chunk's C
+// tokens back to back (R1), so a layer of a fully covered chunk is ONE contiguous 2*C*S_tok run
+// (256 KiB for Llama-8B at C=64).  The copy engines read such runs at up to 98 % of the link
+// (cudaMemcpyBatchAsync of 256 KiB copies over 4 streams, profiles/r01/ce_probe.jsonl) where
+// SM-issued reads top out at 92.6 %.  Each run lands in an HBM staging slot laid out exactly like
+// a compact host tier with one layer (slot j = [K rows][V rows] of C tokens), so the unchanged LDG
+// kernel scatters it to the pages with chunk index = slot index.  Two slots alternate so the copy
+// engines fill one while the SMs scatter the other.
+struct ChunkPos {
+  int32_t req;      // request index
+  int32_t cq;       // position in the request's chunk list
+  int32_t lo, cnt;  // tokens [lo, lo+cnt) of the chunk
+  int32_t i0;       // index of the first of them within the request
+};
+
+struct Piece {
+  size_t first, count;  // chunk positions [first, first+count) -> staging slots 0..count-1
+};
+
+constexpr size_t kStageTarget = size_t(64) << 20;   // bytes per staging slot
+constexpr int kDefaultCtasScatter = 4;   // 2: 53.6-54.0, 4: 54.1-54.2, 8: 54.2-54.4 GB/s
+
+static int ensure_dma(strata_pool* p, size_t slot_bytes, int64_t slots) {
+  cudaError_t e;
+  if (!p->cs[0]) {
+    if (const char* v = getenv("STRATA_COPY_STREAMS"))
+      p->ncs = std::max(1, std::min(strata_pool::kCopyStreams, atoi(v)));
+    for (auto& c : p->cs)
+      if ((e = cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking))) return cuda_fail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+    for (int s = 0; s < 2; ++s) {
+      if ((e = cudaEventCreateWithFlags(&p->ev_slot[s], cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+      for (auto& ev : p->ev_copy[s])
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+    }
+  }
+  if (p->stage_bytes < slot_bytes) {
+    for (auto& b : p->stage) {
+      if (b) cudaFree(b);
+      b = nullptr;
+    }
+    p->stage_bytes = 0;
+    for (auto& b : p->stage)
+      if ((e = cudaMalloc(&b, slot_bytes))) return fail(STRATA_ERR_OOM, "cudaMalloc(staging %zu): %s", slot_bytes,
+                                                        cudaGetErrorString(e));
+    p->stage_bytes = slot_bytes;
+  }
+  if (p->slot_cap < slots) {
+    if (p->slot_ids) cudaFree(p->slot_ids);
+    p->slot_ids = nullptr;
+    p->slot_cap = 0;
+    std::vector<int32_t> iota(static_cast<size_t>(slots));
+    for (int64_t i = 0; i < slots; ++i) iota[i] = static_cast<int32_t>(i);
+    if ((e = cudaMalloc(&p->slot_ids, iota.size() * 4))) return cuda_fail(e, "cudaMalloc(slot ids)");
+    if ((e = cudaMemcpy(p->slot_ids, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice)))
+      return cuda_fail(e, "cudaMemcpy(slot ids)");
+    p->slot_cap = slots;
+  }
+  return STRATA_OK;
+}
+
+void free_dma(strata_pool* p) {
+  for (auto& b : p->stage)
+    if (b) cudaFree(b);
+  if (p->slot_ids) cudaFree(p->slot_ids);
+  for (auto& c : p->cs)
+    if (c) cudaStreamDestroy(c);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  for (int s = 0; s < 2; ++s) {
+    if (p->ev_slot[s]) cudaEventDestroy(p->ev_slot[s]);
+    for (auto& ev : p->ev_copy[s])
+      if (ev) cudaEventDestroy(ev);
+  }
+}
+
+// Submit a copy list over the pool's copy streams (contiguous shares, one batch call each).
+static cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sz,
+                          int dir, int slot) {
+  cudaMemcpyAttributes attr;
+  memset(&attr, 0, sizeof attr);
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.srcLocHint.type = dir == 0 ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
+  attr.srcLocHint.id = dir == 0 ? 0 : p->d.device;
+  attr.dstLocHint.type = dir == 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
+  attr.dstLocHint.id = dir == 0 ? p->d.device : 0;
+  const size_t n = dst.size();
+  const int ns = p->ncs;
+  // cudaMemcpyBatchAsync refuses stream capture; under capture the copies become plain memcpy nodes
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaError_t e0 = cudaStreamIsCapturing(p->cs[0], &cap);
+  if (e0 != cudaSuccess) return e0;
+  const cudaMemcpyKind kind = dir == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  for (int c = 0; c < ns; ++c) {
+    const size_t lo = n * c / ns, hi = n * (c + 1) / ns;
+    if (hi > lo && cap == cudaStreamCaptureStatusActive) {
+      for (size_t i = lo; i < hi; ++i) {
+        cudaError_t e = cudaMemcpyAsync(dst[i], src[i], sz[i], kind, p->cs[c]);
+        if (e != cudaSuccess) return e;
+      }
+    } else if (hi > lo) {
+      size_t idx = 0, fail_idx = 0;
+      cudaError_t e = cudaMemcpyBatchAsync(dst.data() + lo, src.data() + lo, sz.data() + lo, hi - lo, &attr, &idx, 1,
+                                           &fail_idx, p->cs[c]);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(p->ev_copy[slot][c], p->cs[c]);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata::XferParams xp, cudaStream_t s,
+                 int dir, int slot_ev) {
+  if (!x->host_chunks_host && plan.total_tokens > 0)
+    return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
+  const int64_t C = p->d.chunk_tokens, P = p->d.page_size, tok = p->tok_bytes;
+  const int L = p->d.num_layers;
+  // chunk positions of the call, request by request
+  std::vector<ChunkPos> pos;
+  for (int32_t r : plan.reqs) {
+    const int64_t n = x->num_tokens[r];
+    const int64_t oc = x->chunk_offset ? x->chunk_offset[r] : 0;
+    int64_t i = 0;
+    for (int32_t cq = 0; i < n; ++cq) {
+      const int64_t lo = cq == 0 ? oc : 0;
+      const int64_t cnt = std::min(C - lo, n - i);
+      const int64_t hc = x->host_chunks_host[x->chunk_start[r] + cq];
+      if (hc < 0 || hc >= p->d.num_chunks) return fail(STRATA_ERR_INDEX_RANGE, "host chunk %lld out of range", (long long)hc);
+      pos.push_back({r, cq, static_cast<int32_t>(lo), static_cast<int32_t>(cnt), static_cast<int32_t>(i)});
+      i += cnt;
+    }
+  }
+  const size_t unit = static_cast<size_t>(2 * C * tok);             // one chunk-layer: K rows, V rows
+  // layers per copy run.  Loads keep per-layer granularity (grouping does not raise H2D throughput,
+  // profiles/r01/sweep_groups*.jsonl); offloads ("backup", a non-critical path) group
+  // layers until a run is >= 128 KiB, which D2H copies need (70B TP=8 rank: 44.6 -> 55.8 GB/s).
+  int G = x->layer_group;
+  if (G <= 0)
+    G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + 2 * C * tok - 1) / (2 * C * tok)));
+  G = std::max(1, std::min(G, std::max(1, x->layer_end - x->layer_begin)));
+  const size_t gunit = unit * static_cast<size_t>(G);                 // staging bytes per chunk
+  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), kStageTarget / gunit));
+  // pieces: <= per_piece chunk positions and <= kMaxReqsPerLaunch requests each
+  std::vector<Piece> pieces;
+  for (size_t k = 0; k < pos.size();) {
+    Piece pc{k, 0};
+    int nreq = 0;
+    int32_t last = -1;
+    while (k < pos.size() && pc.count < per_piece) {
+      if (pos[k].req != last) {
+        if (nreq == kMaxReqsPerLaunch) break;
+        ++nreq;
+        last = pos[k].req;
+      }
+      ++pc.count;
+      ++k;
+    }
+    pieces.push_back(pc);
+  }
+  int rc = ensure_dma(p, per_piece * gunit, static_cast<int64_t>(per_piece));
+  if (rc) return rc;
+
+  cudaError_t e;
+  const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
+  const int unroll = threads > 512 ? 4 : kDefaultUnroll;
+  xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows
+  const int ctas = x->num_ctas ? x->num_ctas : kDefaultCtasScatter;
+  // staging slot j holds chunk position j's G layers: [G][K,V][C][H][D], a compact host tier
+  xp.chunk_bytes = static_cast<int64_t>(gunit);
+  xp.kv_off = C * tok;
+  xp.host_chunks = p->slot_ids;
+
+  if ((e = cudaEventRecord(p->ev_fork, s))) return cuda_fail(e, "cudaEventRecord");
+  for (int ci = 0; ci < p->ncs; ++ci)
+    if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+  std::vector<void*> dst, src;
+  std::vector<size_t> sz;
+  int64_t i = 0;
+  int last_slot = 0;
+  auto layer_event = [&](int32_t l) { return p->events[size_t(slot_ev) * (L + 1) + 1 + l]; };
+  for (int32_t lg = x->layer_begin; lg < x->layer_end; lg += G) {
+    const int gl = std::min<int>(G, x->layer_end - lg);   // layers in this group
+    for (const Piece& pc : pieces) {
+      const bool last_piece = &pc == &pieces.back();
+      const int slot = static_cast<int>(i & 1);
+      char* stage = p->stage[slot];
+      // copy list of this piece for layers [lg, lg+gl) (host <-> staging slot)
+      dst.clear();
+      src.clear();
+      sz.clear();
+      for (size_t j = 0; j < pc.count; ++j) {
+        const ChunkPos& cp = pos[pc.first + j];
+        const int64_t hc = x->host_chunks_host[x->chunk_start[cp.req] + cp.cq];
+        char* h = p->host + hc * p->chunk_bytes + int64_t(lg) * 2 * C * tok;
+        char* d = stage + j * gunit;
+        auto add = [&](int64_t off, int64_t bytes) {
+          dst.push_back(dir == 0 ? d + off : h + off);
+          src.push_back(dir == 0 ? h + off : d + off);
+          sz.push_back(static_cast<size_t>(bytes));
+        };
+        if (cp.lo == 0 && cp.cnt == C) {
+          add(0, gl * 2 * C * tok);                    // the group's K,V runs are adjacent: one copy
+        } else {
+          for (int g = 0; g < gl; ++g) {
+            add(g * 2 * C * tok + cp.lo * tok, cp.cnt * tok);        // K rows of layer lg+g
+            add(g * 2 * C * tok + (C + cp.lo) * tok, cp.cnt * tok);  // V rows
+          }
+        }
+      }
+      // request table of the piece: sub-requests addressing staging slots
+      strata::ReqTable& rt = xp.rt;
+      rt.n = 0;
+      int32_t acc = 0;
+      for (size_t j = 0; j < pc.count; ++j) {
+        const ChunkPos& cp = pos[pc.first + j];
+        if (j == 0 || cp.req != pos[pc.first + j - 1].req) {
+          const int k = rt.n++;
+          const int64_t op = x->page_offset ? x->page_offset[cp.req] : 0;
+          const int64_t pi0 = op + cp.i0;
+          rt.tok_end[k] = acc;
+          rt.chunk_base[k] = static_cast<int32_t>(j);
+          rt.off_c[k] = cp.lo;
+          rt.page_base[k] = static_cast<int32_t>(x->page_start[cp.req] + pi0 / P);
+          rt.off_p[k] = static_cast<int32_t>(pi0 % P);
+        }
+        acc += cp.cnt;
+        rt.tok_end[rt.n - 1] = acc;
+      }
+      xp.ntok = acc;
+      xp.host = stage;
+      const int64_t groups = (2LL * acc + xp.rows_per_group - 1) / xp.rows_per_group;
+      const int c = static_cast<int>(std::min<int64_t>(ctas, (groups * 32 + threads - 1) / threads));
+      // one scatter / gather launch per layer of the group over the slot's layer sub-blocks
+      auto launch_group = [&](int kdir) -> cudaError_t {
+        for (int g = 0; g < gl; ++g) {
+          xp.kbase = static_cast<char*>(p->k[lg + g]);
+          xp.vbase = static_cast<char*>(p->v[lg + g]);
+          xp.layer_off = int64_t(g) * 2 * C * tok;
+          cudaError_t le = strata::launch_ldg(xp, kdir, c, threads, unroll, s);
+          if (le != cudaSuccess) return le;
+          ++p->counters.kernel_launches;
+          // loads: layer lg+g is complete once its scatter of the group's last piece has run
+          if (kdir == 0 && last_piece && (le = cudaEventRecord(layer_event(lg + g), s))) return le;
+        }
+        return cudaSuccess;
+      };
+      const int ncs = p->ncs;
+      if (dir == 0) {
+        // copies into the slot (after its previous scatter), then the scatters on the caller's stream
+        if (i >= 2)
+          for (int ci = 0; ci < ncs; ++ci)
+            if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        for (int ci = 0; ci < ncs; ++ci)
+          if ((e = cudaStreamWaitEvent(s, p->ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = launch_group(0))) return cuda_fail(e, "scatter kernel launch");
+        if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
+      } else {
+        // gathers into the slot (after its previous copies drained), then copies to the host tier
+        if (i >= 2)
+          for (int ci = 0; ci < ncs; ++ci)
+            if ((e = cudaStreamWaitEvent(s, p->ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = launch_group(1))) return cuda_fail(e, "gather kernel launch");
+        if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
+        for (int ci = 0; ci < ncs; ++ci)
+          if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+      }
+      p->counters.dma_copies += static_cast<int64_t>(dst.size());
+      last_slot = slot;
+      ++i;
+    }
+    if (dir == 0 && pieces.empty()) {
+      for (int g = 0; g < gl; ++g)
+        if ((e = cudaEventRecord(layer_event(lg + g), s))) return cuda_fail(e, "cudaEventRecord");
+    } else if (dir == 1) {
+      // host bytes of the group are written once every copy stream has passed its last piece
+      if (!pieces.empty())
+        for (int c = 1; c < p->ncs; ++c)
+          if ((e = cudaStreamWaitEvent(p->cs[0], p->ev_copy[last_slot][c], 0)))
+            return cuda_fail(e, "cudaStreamWaitEvent");
+      for (int g = 0; g < gl; ++g)
+        if ((e = cudaEventRecord(layer_event(lg + g), p->cs[0]))) return cuda_fail(e, "cudaEventRecord");
+    }
+  }
+  if (dir == 1 && i > 0)  // join: the caller's stream is ordered after every copy
+    for (int ci = 0; ci < p->ncs; ++ci)
+      if ((e = cudaStreamWaitEvent(s, p->ev_copy[last_slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+  return STRATA_OK;
+}
+
+}  // namespace strata

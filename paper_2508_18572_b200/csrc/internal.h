@@ -1,5 +1,6 @@
-// internal.h — libstrata internals shared by the API layer (api.cpp, baselines.cpp) and the
-// sm_100a kernels (kernels.cu).  Not part of the ABI; see include/strata.h for the contract.
+// internal.h — libstrata internals shared by the host side (api.cpp, transfer.cpp, dma.cpp,
+// baselines.cpp, disk.cpp) and the sm_100a kernels (kernels.cu).  Not part of the ABI; see
+// include/strata.h for the contract.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -124,3 +125,59 @@ struct strata_pool {
   cudaEvent_t ev_slot[2] = {nullptr, nullptr};                 // staging slot reusable
   cudaEvent_t ev_copy[2][kCopyStreams] = {};                   // a slot's copies done, per stream
 };
+
+// ------------------------------------------------------------------------------------------------
+// Shared between api.cpp (ABI surface), transfer.cpp (validation, planning, kernel engines) and
+// dma.cpp (copy-engine engine).
+namespace strata {
+
+// Records a formatted message as strata_last_error() and returns `code` (api.cpp).
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int cuda_fail(cudaError_t e, const char* what);
+
+// Makes `dev` current for the scope, restoring the caller's device afterwards.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// Per-call plan: the non-empty requests, split into launches (batches) of <= kMaxReqsPerLaunch.
+struct Batch {
+  int32_t first, count;     // requests [first, first+count) among the non-empty ones
+  int32_t ntok;
+};
+
+struct Plan {
+  std::vector<int32_t> reqs;   // indices of requests with tokens
+  std::vector<Batch> batches;
+  int64_t total_tokens = 0;
+};
+
+// Defaults chosen on B200 measurements.
+// The paper's quota: 2 CTAs x 1024 threads.  On B200 that moves 50.3 GB/s (90.7 % of
+// the link) with 0.8 % prefill-GEMM and 10.8 % decode slowdown (profiles/r01/interference2.jsonl).
+constexpr int kDefaultCtasLdg = 2;
+constexpr int kDefaultThreadsLdg = 1024;   // host-read throughput of an SM scales with its warps
+constexpr int64_t kDmaMinLayerBytes = int64_t(4) << 20;
+constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;
+constexpr int kDefaultUnroll = 8;
+constexpr int kDefaultCtasTma = 2;   // warp-specialised ring: 51.0 GB/s at 2 CTAs (sweep_tma_ws15.jsonl)
+constexpr int kTmaStageTarget = 32 << 10;
+
+int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan);                     // transfer.cpp
+void fill_table(const strata_xfer* x, const Plan& plan, const Batch& b, ReqTable& rt);        // transfer.cpp
+int ilog2_exact(int v);                                                                       // transfer.cpp
+int transfer(strata_pool* p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir); // transfer.cpp
+int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, XferParams xp, cudaStream_t s,
+                 int dir, int slot_ev);                                                       // dma.cpp
+void free_dma(strata_pool* p);                                                                // dma.cpp
+
+}  // namespace strata
