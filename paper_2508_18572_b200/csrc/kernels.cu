@@ -129,6 +129,22 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __gri
     const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
     const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
     const int nvec = nr * p.vpt;
+    if (CONTIG && p.row_wide) {
+      // rows of >= 32*U vectors (>= 2 KiB for U=4): every warp iteration stays inside one row, so
+      // the row's two addresses are broadcast once per iteration, not once per vector
+      for (int base = 0; base < nvec; base += 32 * U) {
+        const int rl = p.vpt_shift >= 0 ? (base >> p.vpt_shift) : (base / p.vpt);
+        const int w0 = base - rl * p.vpt + lane;
+        const char* s = reinterpret_cast<const char*>(__shfl_sync(kFull, my_src, rl)) + w0 * 16;
+        char* d = reinterpret_cast<char*>(__shfl_sync(kFull, my_dst, rl)) + w0 * 16;
+        int4 v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) v[j] = ld_stream(s + j * 512);
+#pragma unroll
+        for (int j = 0; j < U; ++j) st_vec(d + j * 512, v[j]);
+      }
+      continue;
+    }
     for (int base = 0; base < nvec; base += 32 * U) {
       int4 v[U];
 #pragma unroll
