@@ -180,7 +180,6 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;
   xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows
-  xp.row_wide = xp.vpt % (32 * unroll) == 0;
   const int ctas = x->num_ctas ? x->num_ctas : kDefaultCtasScatter;
   // staging slot j holds chunk position j's G layers: [G][K,V][C][H][D], a compact host tier
   xp.chunk_bytes = static_cast<int64_t>(gunit);

@@ -43,8 +43,6 @@ struct XferParams {
   int32_t tma_stages;           // TMA engine: pipeline depth
   int32_t tma_stage_bytes;      // TMA engine: bytes per stage (>= tma_rows * tok_bytes)
   int32_t c_shift, p_shift;     // log2(C), log2(P) when powers of two, else -1
-  int32_t row_wide;             // LDG engine: vpt % (32*U) == 0, a warp iteration never spans rows
-  int32_t pad0_;
   int64_t chunk_bytes;          // L*2*C*S_tok
   int64_t layer_off;            // byte offset of (layer, K) inside a host chunk: l*2*C*S_tok
   int64_t kv_off;               // byte offset from K to V inside a chunk layer: C*S_tok

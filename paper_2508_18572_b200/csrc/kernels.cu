@@ -15,7 +15,7 @@
 //                       with U independent 16-byte LDG/STG per lane, addresses broadcast by
 //                       __shfl_sync.  Also the scatter / gather of the DMA engine (HBM staging).
 //   tma_ws_load_kernel  zero-copy TMA: one producer warp issues one cp.async.bulk per contiguous
-//                       host run into a shared-memory ring; 4 consumer warps drain it to the pages.
+//                       host run into a shared-memory ring; 15 consumer warps drain it to the pages.
 //   tma_kernel          zero-copy TMA, single warp, bulk copies on both sides of the ring.
 // Measured on the B200 box (profiles/r01): SM-issued host reads top out at 51.4 GB/s (92.6 % of the
 // 55.5 GB/s pinned memcpy) whatever the instruction or cache hint; per SM they scale with resident
@@ -129,22 +129,6 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __gri
     const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
     const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
     const int nvec = nr * p.vpt;
-    if (CONTIG && p.row_wide) {
-      // rows of >= 32*U vectors (>= 2 KiB for U=4): every warp iteration stays inside one row, so
-      // the row's two addresses are broadcast once per iteration, not once per vector
-      for (int base = 0; base < nvec; base += 32 * U) {
-        const int rl = p.vpt_shift >= 0 ? (base >> p.vpt_shift) : (base / p.vpt);
-        const int w0 = base - rl * p.vpt + lane;
-        const char* s = reinterpret_cast<const char*>(__shfl_sync(kFull, my_src, rl)) + w0 * 16;
-        char* d = reinterpret_cast<char*>(__shfl_sync(kFull, my_dst, rl)) + w0 * 16;
-        int4 v[U];
-#pragma unroll
-        for (int j = 0; j < U; ++j) v[j] = ld_stream(s + j * 512);
-#pragma unroll
-        for (int j = 0; j < U; ++j) st_vec(d + j * 512, v[j]);
-      }
-      continue;
-    }
     for (int base = 0; base < nvec; base += 32 * U) {
       int4 v[U];
 #pragma unroll

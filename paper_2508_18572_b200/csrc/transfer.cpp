@@ -234,7 +234,6 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;   // U=8 is compiled for <= 512 threads
   xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows (amortised index math)
-  xp.row_wide = xp.vpt % (32 * unroll) == 0;
   int ctas = x->num_ctas ? x->num_ctas : (engine == STRATA_ENGINE_LDG ? kDefaultCtasLdg : kDefaultCtasTma);
   // small token rows shrink a TMA stage (<= 32 rows); keep ~64 KiB per stage-CTA in flight by
   // spreading over more CTAs (70B TP=8: 256 B rows -> 8 KiB stages -> 16 CTAs)
