@@ -1,0 +1,41 @@
+"""bench.py's JSON contract, checked on CPU: the reference arm (the oracle on the host cores) runs
+without a GPU, and the committed round-1 bench line carries every key the driver reads."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def test_reference_arm_runs_on_cpu():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "tiny",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "GB/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["workload"] == "tiny"
+    metric = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+    assert d["metric"] == metric
+
+
+def test_committed_bench_line_is_complete():
+    d = json.load(open(os.path.join(ROOT, "profiles", "r01", "bench.json")))
+    assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
+    assert d["config"]["workload"] == "llama8b_32k" and d["n_gpus"] == 1
+    rf = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(rf)
+    assert 0 < rf["frac"] <= 1.05
+    assert d["cpu_baseline"]["kind"] == "oracle"
+    assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])
+    assert d["gpu_launches"] > 0
+    assert d["clocks"]["sm_mhz"] > 0 and not ({"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+                                               & set(d["clocks"]["reasons"]))
+    assert d["warmup"] >= 3

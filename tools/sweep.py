@@ -56,10 +56,13 @@ def main():
     ap.add_argument("--tag", default="")
     ap.add_argument("--threads", type=int, default=0, help="LDG engine threads per CTA (0 = default)")
     ap.add_argument("--groups", default="0", help="DMA layer_group values to sweep")
+    ap.add_argument("--host-chunks", type=int, default=0, help="override the host tier capacity (chunks)")
     args = ap.parse_args()
     io = torch.cuda.Stream()
     for P in [int(x) for x in args.pages.split(",")]:
         over = {"L": args.layers} if args.layers else {}
+        if args.host_chunks:
+            over["num_chunks"] = args.host_chunks
         g = kvgen.geometry(args.config, P=P, **over)
         n = kvgen.CONFIGS[args.config]["n"]
         q = kvgen.make_requests(kvgen.rng_for(1), n, g.P, g.C, g.num_pages, g.num_chunks, frag=args.frag,
@@ -74,7 +77,8 @@ def main():
         reqs = st.Requests.from_kvgen(q)
         nbytes = 2 * g.L * q.total_tokens * g.token_bytes
         base = {"config": args.config, "P": P, "L": g.L, "tokens": q.total_tokens, "bytes": nbytes, "frag": args.frag,
-                "chunk_frag": args.chunk_frag, "flags": args.flags, "tag": args.tag}
+                "chunk_frag": args.chunk_frag, "flags": args.flags, "tag": args.tag,
+                "host_tier_bytes": g.host_bytes}
         for eng in [int(x) for x in args.engines.split(",")]:
           for G in ([int(x) for x in args.groups.split(",")] if eng == 4 else [0]):
             for c in [int(x) for x in args.ctas.split(",")]:
