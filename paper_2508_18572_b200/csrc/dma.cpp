@@ -155,7 +155,9 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + 2 * C * tok - 1) / (2 * C * tok)));
   G = std::max(1, std::min(G, std::max(1, x->layer_end - x->layer_begin)));
   const size_t gunit = unit * static_cast<size_t>(G);                 // staging bytes per chunk
-  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), kStageTarget / gunit));
+  size_t stage_target = kStageTarget;
+  if (const char* v = getenv("STRATA_STAGE_MB")) stage_target = std::max<size_t>(1, strtoull(v, nullptr, 10)) << 20;
+  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), stage_target / gunit));
   // pieces: <= per_piece chunk positions and <= kMaxReqsPerLaunch requests each
   std::vector<Piece> pieces;
   for (size_t k = 0; k < pos.size();) {
