@@ -210,10 +210,20 @@ def main():
     import paper_2508_18572_b200 as st
 
     rank, world, local = dist_env()
+    # STRATA_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 with gloo for the barrier and
+    # the max-over-ranks reduction, so the N>1 flow runs on a one-GPU box (NCCL refuses two ranks
+    # on one device).  Never used for reported numbers.
+    share = os.environ.get("STRATA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
+    red_dev = "cpu" if share else "cuda"
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     g, q = workload(args, rank, world)
     nb = g.num_pages * g.P * g.token_bytes
@@ -262,7 +272,7 @@ def main():
     # per-layer (= per-launch) durations of the last timed step, from the library's own events
     t_layer = [pool.layer_elapsed_ms(last, l) for l in range(g.L)]
     launch_ms = [t_layer[0]] + [b - a for a, b in zip(t_layer, t_layer[1:])]
-    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    t = torch.tensor([elapsed], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_max = float(t.item())
@@ -302,7 +312,7 @@ def main():
                            non_blocking=True)
         io.synchronize()
     e2e_dt = time.perf_counter() - t0
-    te = torch.tensor([e2e_dt], dtype=torch.float64, device="cuda")
+    te = torch.tensor([e2e_dt], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = bytes_step * world * e2e_steps / float(te.item()) / 1e9
@@ -376,6 +386,7 @@ def main():
             "clocks": clocks.summary(),
             "engine": engine_used, "num_ctas": args.num_ctas or "default",
             "other_engines_gbs": others,
+            "shared_gpu_test_mode": share or None,
             "zero_copy_kernels": zc,
             "per_layer_ms_last_step": [round(x, 4) for x in launch_ms],
         }

@@ -11,7 +11,7 @@ import re
 from typing import List
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstrata.so")
+LIB_PATH = os.environ.get("STRATA_LIB_PATH") or os.path.join(_HERE, "libstrata.so")   # env: A/B builds
 INCLUDE_DIR = os.path.join(os.path.dirname(_HERE), "include")
 
 STRATA_OK = 0

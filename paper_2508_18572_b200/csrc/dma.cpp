@@ -33,8 +33,11 @@ struct Piece {
   size_t first, count;  // chunk positions [first, first+count) -> staging slots 0..count-1
 };
 
-constexpr size_t kStageTarget = size_t(64) << 20;   // bytes per staging slot
-constexpr int kDefaultCtasScatter = 4;   // 2: 53.6-54.0, 4: 54.1-54.2, 8: 54.2-54.4 GB/s
+// bytes per staging slot (2 slots) and scatter quota: 64 MiB / 4 CTAs 54.2, 64 / 8 54.4,
+// 128 / 8 54.7, 256 / 8 54.7 GB/s (profiles/r01/stage.jsonl): fewer, larger pieces leave fewer
+// inter-piece event waits on the copy streams and a shorter scatter tail.
+constexpr size_t kStageTarget = size_t(128) << 20;
+constexpr int kDefaultCtasScatter = 8;
 
 static int ensure_dma(strata_pool* p, size_t slot_bytes, int64_t slots) {
   cudaError_t e;
