@@ -230,7 +230,9 @@ class Ctl:
 
     # ---------------------------------------------------------------- public tree operations
     def insert(self, tokens, tier: int, now: float) -> List[int]:
-        """Make `tokens` resident on `tier`; return every token's slot there (SPEC insert)."""
+        """Make `tokens` resident on `tier`; return every token's slot there (SPEC insert).
+        Replaces both plans, like a scheduling round (its evictions' write-backs)."""
+        self.load_pairs, self.offload_pairs = [], []
         nodes, i = self._align(tokens)
         pool, unit = (self.dpool, self.P) if tier == DEVICE else (self.hpool, self.C)
         attr = "dev" if tier == DEVICE else "host"
