@@ -20,23 +20,25 @@ __all__ = ["shared_context_trace", "conversation_trace", "random_prefix_family"]
 
 def shared_context_trace(rng: np.random.Generator, docs: int, questions: int, doc_len: int,
                          q_len: Tuple[int, int], vocab: int = 32000, order: str = "min",
-                         system_prompt: int = 0) -> List[List[int]]:
+                         system_prompt: int = 0, return_docs: bool = False):
     """Requests = [system prompt] + document + question.
 
     order "min": the questions of a document arrive back to back (minimum cache distance);
     "max": round-robin over documents (maximum distance); "random": shuffled.
+    return_docs: also return each document's context (system prompt + document).
     """
     sp = rng.integers(0, vocab, system_prompt).tolist()
     bodies = [rng.integers(0, vocab, doc_len).tolist() for _ in range(docs)]
     reqs = [[sp + bodies[d] + rng.integers(0, vocab, int(rng.integers(q_len[0], q_len[1] + 1))).tolist()
              for _ in range(questions)] for d in range(docs)]
     if order == "min":
-        return [r for d in range(docs) for r in reqs[d]]
-    if order == "max":
-        return [reqs[d][q] for q in range(questions) for d in range(docs)]
-    flat = [r for d in range(docs) for r in reqs[d]]
-    perm = rng.permutation(len(flat))
-    return [flat[i] for i in perm]
+        out = [r for d in range(docs) for r in reqs[d]]
+    elif order == "max":
+        out = [reqs[d][q] for q in range(questions) for d in range(docs)]
+    else:
+        flat = [r for d in range(docs) for r in reqs[d]]
+        out = [flat[i] for i in rng.permutation(len(flat))]
+    return (out, [sp + b for b in bodies]) if return_docs else out
 
 
 def conversation_trace(rng: np.random.Generator, convs: int, rounds: int, first_len: Tuple[int, int],
