@@ -130,6 +130,7 @@ void free_host(strata_pool* p) {
 
 void destroy(strata_pool* p) {
   strata::free_dma(p);
+  strata::free_fused(p);
   for (cudaEvent_t e : p->events)
     if (e) cudaEventDestroy(e);
   if (p->bitmap) cudaFree(p->bitmap);
@@ -258,6 +259,7 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
     destroy(p);
     return cuda_fail(e, "cudaFuncSetAttribute(TMA smem)");
   }
+  strata::ensure_fused(p);   // setup only: keeps allocation and stream creation out of timed calls
   *out = p;
   return STRATA_OK;
 }

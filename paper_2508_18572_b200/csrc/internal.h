@@ -71,8 +71,22 @@ struct ValidateParams {
   ReqTable rt;
 };
 
+// One launch for every layer of an LDG operation (kernels.cu ldg_fused_kernel).
+constexpr int kMaxFusedLayers = 128;
+struct FusedParams {
+  XferParams x;                 // geometry, index lists, request table (kbase/vbase/layer_off unused)
+  int32_t l0, l1;               // layer range
+  uint32_t epoch;               // published to flags[l] when layer l is complete
+  int32_t total_warps;          // warps in the grid (each arrives once per layer)
+  uint32_t* counters;           // [L] arrival counters of this op slot (0 on entry, reset by the kernel)
+  uint32_t* flags;              // [L] completion flags of this op slot
+  char* kb[kMaxFusedLayers];    // per-layer K / V bases
+  char* vb[kMaxFusedLayers];
+};
+
 // Kernel launchers (kernels.cu).  dir: 0 = load (host -> device), 1 = offload (device -> host).
 cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s);
+cudaError_t launch_ldg_fused(const FusedParams& p, int dir, int ctas, int threads, cudaStream_t s);
 // warp_specialized (load only): 1 TMA producer warp + LSU consumer warps; else one bulk-only warp.
 cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s);
 cudaError_t launch_validate(const ValidateParams& v, cudaStream_t s);
@@ -124,6 +138,11 @@ struct strata_pool {
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_slot[2] = {nullptr, nullptr};                 // staging slot reusable
   cudaEvent_t ev_copy[2][kCopyStreams] = {};                   // a slot's copies done, per stream
+  // fused LDG operations (lazy): per op slot, L arrival counters + L layer flags (device), and a side
+  // stream that turns each flag into the layer's event (cuStreamWaitValue32 + cudaEventRecord)
+  uint32_t* fused_sync = nullptr;     // [kEventRing][2][L]
+  cudaStream_t side[strata::kEventRing] = {};
+  int fused_state = 0;                // 0 untried, 1 ready, -1 unavailable (stream memory ops missing)
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -178,6 +197,8 @@ int ilog2_exact(int v);                                                         
 int transfer(strata_pool* p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir); // transfer.cpp
 int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, XferParams xp, cudaStream_t s,
                  int dir, int slot_ev);                                                       // dma.cpp
-void free_dma(strata_pool* p);                                                                // dma.cpp
+void free_dma(strata_pool* p);
+void free_fused(strata_pool* p);
+bool ensure_fused(strata_pool* p);   // fused-LDG resources; false: unavailable (per-layer path) transfer.cpp                                                              // transfer.cpp                                                                // dma.cpp
 
 }  // namespace strata

@@ -78,13 +78,17 @@ __device__ __forceinline__ RowIdx row_none() {
   return x;
 }
 
-__device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x, char*& hp, char*& dp) {
+__device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x, char* kbase, char* vbase,
+                                           int64_t layer_off, char*& hp, char*& dp) {
   // host: chunk hc, layer l, kv, token cr            (page-first)
-  hp = p.host + static_cast<int64_t>(x.hc) * p.chunk_bytes + p.layer_off + x.kv * p.kv_off +
+  hp = p.host + static_cast<int64_t>(x.hc) * p.chunk_bytes + layer_off + x.kv * p.kv_off +
        static_cast<int64_t>(x.cr) * p.tok_bytes;
   // device: page pg, offset pr of this layer's K/V  (layer-first paged pool)
-  dp = (x.kv ? p.vbase : p.kbase) + static_cast<int64_t>(x.pg) * p.page_stride +
+  dp = (x.kv ? vbase : kbase) + static_cast<int64_t>(x.pg) * p.page_stride +
        static_cast<int64_t>(x.pr) * p.token_stride;
+}
+__device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x, char*& hp, char*& dp) {
+  row_finish(p, x, p.kbase, p.vbase, p.layer_off, hp, dp);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -103,11 +107,11 @@ __device__ __forceinline__ void st_vec(void* ptr, const int4& v) {
 // ---------------------------------------------------------------------------------------------
 // LDG engine.  DIR 0: host -> device, DIR 1: device -> host.  CONTIG: device rows head-contiguous
 // (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
+// One layer of the LDG engine for this warp: groups warp, warp + nwarps, ...  `nx` holds the
+// already-fetched indices of the warp's first group (identical for every layer).
 template <int U, bool CONTIG, int DIR>
-__global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __grid_constant__ XferParams p) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+__device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char* vbase, int64_t layer_off,
+                                          RowIdx nx, int64_t warp, int64_t nwarps, int lane) {
   const int64_t nrows = 2LL * p.ntok;
   const int RG = p.rows_per_group;
   const int64_t ngroups = (nrows + RG - 1) / RG;
@@ -117,7 +121,6 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __gri
     const int64_t row = gi * RG + lane;
     return (gi < ngroups && lane < RG && row < nrows) ? row_fetch(p, row) : row_none();
   };
-  RowIdx nx = fetch(warp);
   for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
     const int64_t row0 = gi * RG;
     const int nr = static_cast<int>(min(static_cast<int64_t>(RG), nrows - row0));
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __gri
     nx = fetch(gi + nwarps);
     char* hp = nullptr;
     char* dp = nullptr;
-    if (cur.kv >= 0) row_finish(p, cur, hp, dp);   // addresses by lane, broadcast below
+    if (cur.kv >= 0) row_finish(p, cur, kbase, vbase, layer_off, hp, dp);   // by lane, broadcast below
     const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
     const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
     const int nvec = nr * p.vpt;
@@ -164,6 +167,65 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __gri
           }
           st_vec(a, v[j]);
         }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ RowIdx ldg_first(const XferParams& p, int64_t warp, int lane) {
+  const int64_t nrows = 2LL * p.ntok;
+  const int64_t ngroups = (nrows + p.rows_per_group - 1) / p.rows_per_group;
+  const int64_t row = warp * p.rows_per_group + lane;
+  return (warp < ngroups && lane < p.rows_per_group && row < nrows) ? row_fetch(p, row) : row_none();
+}
+
+// LDG engine, one layer per launch.  DIR 0: host -> device, DIR 1: device -> host.  CONTIG: device
+// rows head-contiguous (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
+template <int U, bool CONTIG, int DIR>
+__global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __grid_constant__ XferParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  ldg_layer<U, CONTIG, DIR>(p, p.kbase, p.vbase, p.layer_off, ldg_first(p, warp, lane), warp, nwarps, lane);
+}
+
+// LDG engine, every layer of the operation in ONE launch (the persistent variant):
+// warps flow from layer l into layer l+1 without a kernel boundary, and layer l's completion is a
+// device flag.  Each warp, after its share of layer l, fences its stores (system scope: offload
+// rows land in host memory) and arrives on counters[l]; the last arriver resets the counter for the
+// slot's next operation and publishes `epoch` to flags[l].  The host side turns each flag into the
+// layer's CUDA event with cuStreamWaitValue32 + cudaEventRecord on the op slot's side stream.
+// Loads land in HBM and are consumed by GPU work: GPU-scope fences.  Offloads land in host memory,
+// which the host may read after the event: system scope.
+template <int DIR>
+__device__ __forceinline__ void layer_fence() {
+  if (DIR == 0) __threadfence();
+  else __threadfence_system();
+}
+template <int DIR>
+__device__ __forceinline__ void st_release(uint32_t* a, uint32_t v) {
+  if (DIR == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
+  else asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
+}
+
+template <int U, bool CONTIG, int DIR>
+__global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const __grid_constant__ FusedParams fp) {
+  const XferParams& p = fp.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const RowIdx first = ldg_first(p, warp, lane);
+  const int64_t layer_step = 2LL * p.C * p.tok_bytes;
+  for (int l = fp.l0; l < fp.l1; ++l) {
+    ldg_layer<U, CONTIG, DIR>(p, fp.kb[l], fp.vb[l], int64_t(l) * layer_step, first, warp, nwarps, lane);
+    __syncwarp();
+    if (lane == 0) {
+      layer_fence<DIR>();
+      const uint32_t prev = atomicAdd(fp.counters + l, 1u);
+      if (prev == static_cast<uint32_t>(fp.total_warps - 1)) {
+        fp.counters[l] = 0;
+        layer_fence<DIR>();
+        st_release<DIR>(fp.flags + l, fp.epoch);
       }
     }
   }
@@ -472,6 +534,12 @@ cudaError_t ldg_launch(const XferParams& p, int ctas, int threads, cudaStream_t 
   return cudaGetLastError();
 }
 
+template <int U, bool CONTIG, int DIR>
+cudaError_t ldg_fused_launch(const FusedParams& p, int ctas, int threads, cudaStream_t s) {
+  ldg_fused_kernel<U, CONTIG, DIR><<<ctas, threads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <int DIR, bool CONTIG>
 cudaError_t tma_launch(const XferParams& p, int ctas, cudaStream_t s) {
   const int smem = tma_buf_offset(p.tma_stages) + p.tma_stages * p.tma_stage_bytes;
@@ -495,6 +563,20 @@ cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int 
   STRATA_LDG(8)
 #undef STRATA_LDG
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_ldg_fused(const FusedParams& p, int dir, int ctas, int threads, cudaStream_t s) {
+  const bool contig = p.x.head_stride == p.x.head_bytes;
+  if (threads > 512) {
+    if (dir == 0) return contig ? ldg_fused_launch<4, true, 0>(p, ctas, threads, s)
+                                : ldg_fused_launch<4, false, 0>(p, ctas, threads, s);
+    return contig ? ldg_fused_launch<4, true, 1>(p, ctas, threads, s)
+                  : ldg_fused_launch<4, false, 1>(p, ctas, threads, s);
+  }
+  if (dir == 0) return contig ? ldg_fused_launch<8, true, 0>(p, ctas, threads, s)
+                              : ldg_fused_launch<8, false, 0>(p, ctas, threads, s);
+  return contig ? ldg_fused_launch<8, true, 1>(p, ctas, threads, s)
+                : ldg_fused_launch<8, false, 1>(p, ctas, threads, s);
 }
 
 cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s) {

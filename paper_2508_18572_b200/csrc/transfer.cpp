@@ -5,6 +5,7 @@
 // at most kMaxReqsPerLaunch whose tables travel in the kernel parameters, pick the engine and the SM
 // quota ("a small number of large CUDA blocks"), then for every layer l in
 // [l0, l1): launch, and record event (ticket, l) (§4.1: the executor waits per layer).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,6 +16,71 @@
 #include "internal.h"
 
 namespace strata {
+
+namespace {
+
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32Fn g_wait_value32 = nullptr;
+
+// STRATA_LDG_FUSED=0 keeps the one-launch-per-layer LDG path (A/B and fallback testing)
+bool fused_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("STRATA_LDG_FUSED");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// Lazily: per op slot 2*L device words (arrival counters, layer flags) and a side stream; the
+// driver's stream memory operation cuStreamWaitValue32 through the runtime's entry-point query,
+// probed once on a zero flag.  Unavailable -> the per-layer path is used.
+}  // namespace
+
+bool ensure_fused(strata_pool* p) {
+  if (p->fused_state) return p->fused_state > 0;
+  p->fused_state = -1;
+  if (!g_wait_value32) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return false;
+    }
+    g_wait_value32 = reinterpret_cast<WaitValue32Fn>(fn);
+  }
+  const size_t words = size_t(kEventRing) * 2 * p->d.num_layers;
+  if (cudaMalloc(&p->fused_sync, words * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(p->fused_sync, 0, words * sizeof(uint32_t)) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  for (int i = 0; i < kEventRing; ++i)
+    if (cudaStreamCreateWithFlags(&p->side[i], cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+  if (g_wait_value32(reinterpret_cast<CUstream>(p->side[0]), reinterpret_cast<CUdeviceptr>(p->fused_sync), 0,
+                     CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+      cudaStreamSynchronize(p->side[0]) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  p->fused_state = 1;
+  return true;
+}
+
+void free_fused(strata_pool* p) {
+  for (int i = 0; i < kEventRing; ++i)
+    if (p->side[i]) {
+      cudaStreamSynchronize(p->side[i]);
+      cudaStreamDestroy(p->side[i]);
+      p->side[i] = nullptr;
+    }
+  if (p->fused_sync) cudaFree(p->fused_sync);
+  p->fused_sync = nullptr;
+  p->fused_state = 0;
+}
 
 int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan) {
   if (!x) return fail(STRATA_ERR_INVALID_ARG, "xfer is NULL");
@@ -251,6 +317,50 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   };
   e = cudaEventRecord(p->events[size_t(slot) * (L + 1)], s);  // operation start
   if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
+  // One launch for all layers when the call is one request table and not being captured (stream
+  // memory operations are not captured here); layer events come from the device flags.  Measured
+  // (profiles/r01/fused_ab_*.jsonl): +2 % at the default 2 CTAs (51.2 GB/s, 99.4 % of the SM
+  // zero-copy ceiling), +0.5 % at 4, but -3..-7 % with a single CTA, so 1-CTA grids keep the
+  // per-layer launches.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const int64_t fgroups = plan.batches.empty() ? 0
+                              : (2LL * plan.batches[0].ntok + xp.rows_per_group - 1) / xp.rows_per_group;
+  const int fctas = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctas, (fgroups * 32 + threads - 1) / threads)));
+  if (engine == STRATA_ENGINE_LDG && plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 &&
+      fctas >= 2 && L <= kMaxFusedLayers && fused_enabled() && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
+      cap == cudaStreamCaptureStatusNone && ensure_fused(p)) {
+    const Batch& b = plan.batches[0];
+    FusedParams fp;
+    std::memset(&fp, 0, sizeof fp);
+    fp.x = xp;
+    fp.x.ntok = b.ntok;
+    fill_table(x, plan, b, fp.x.rt);
+    const int c = fctas;
+    fp.l0 = x->layer_begin;
+    fp.l1 = x->layer_end;
+    fp.epoch = static_cast<uint32_t>(t);
+    fp.total_warps = c * threads / 32;
+    fp.counters = p->fused_sync + size_t(slot) * 2 * L;
+    fp.flags = fp.counters + L;
+    for (int l = 0; l < L; ++l) {
+      fp.kb[l] = static_cast<char*>(p->k[l]);
+      fp.vb[l] = static_cast<char*>(p->v[l]);
+    }
+    e = strata::launch_ldg_fused(fp, dir, c, threads, s);
+    if (e != cudaSuccess) return op_fail(e, "fused transfer kernel launch");
+    ++p->counters.kernel_launches;
+    cudaStream_t side = p->side[slot];
+    for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
+      if (g_wait_value32(reinterpret_cast<CUstream>(side), reinterpret_cast<CUdeviceptr>(fp.flags + l), fp.epoch,
+                         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return op_fail(cudaErrorUnknown, "cuStreamWaitValue32");
+      e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], side);
+      if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
+    }
+    count_op(p, plan, x, engine);
+    if (ticket) *ticket = t;
+    return STRATA_OK;
+  }
   for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
     xp.kbase = static_cast<char*>(p->k[l]);
     xp.vbase = static_cast<char*>(p->v[l]);
