@@ -22,13 +22,16 @@ namespace {
 using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 WaitValue32Fn g_wait_value32 = nullptr;
 
-// STRATA_LDG_FUSED=0 keeps the one-launch-per-layer LDG path (A/B and fallback testing)
-bool fused_enabled() {
-  static const bool on = [] {
+// STRATA_LDG_FUSED: "0" keeps the one-launch-per-layer LDG path (A/B and fallback testing);
+// "force" fuses 1-CTA grids too (profiling); default: fused from 2 CTAs.
+int fused_mode() {
+  static const int mode = [] {
     const char* v = std::getenv("STRATA_LDG_FUSED");
-    return !(v && v[0] == '0');
+    if (v && v[0] == '0') return 0;
+    if (v && std::strcmp(v, "force") == 0) return 2;
+    return 1;
   }();
-  return on;
+  return mode;
 }
 
 // Lazily: per op slot 2*L device words (arrival counters, layer flags) and a side stream; the
@@ -327,7 +330,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
                               : (2LL * plan.batches[0].ntok + xp.rows_per_group - 1) / xp.rows_per_group;
   const int fctas = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctas, (fgroups * 32 + threads - 1) / threads)));
   if (engine == STRATA_ENGINE_LDG && plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 &&
-      fctas >= 2 && L <= kMaxFusedLayers && fused_enabled() && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
+      (fctas >= 2 || fused_mode() == 2) && L <= kMaxFusedLayers && fused_mode() && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
       cap == cudaStreamCaptureStatusNone && ensure_fused(p)) {
     const Batch& b = plan.batches[0];
     FusedParams fp;
