@@ -243,50 +243,89 @@ struct strata_ctl {
   }
 
   // ------------------------------------------------------------------ eviction (R23)
-  // least recently used candidate; ties broken by the lexicographically smaller path
+  // Victim order: least recent last_access, ties broken by the lexicographically smaller token path.
+  // Paths are compared without materialising them: below their lowest common ancestor two paths
+  // diverge at the first tokens of two sibling edges (radix property); an ancestor's path is a
+  // prefix of its descendants' (smaller).
+  static int depth_of(const Node* n) {
+    int d = 0;
+    for (; n->parent; n = n->parent) ++d;
+    return d;
+  }
+  static bool path_less(const Node* a, const Node* b) {
+    if (a == b) return false;
+    int da = depth_of(a), db = depth_of(b);
+    const Node* x = a;
+    const Node* y = b;
+    bool lifted_a = false;
+    while (da > db) { x = x->parent; --da; lifted_a = true; }
+    while (db > da) { y = y->parent; --db; }
+    if (x == y) return !lifted_a;            // one is the other's ancestor: the ancestor is smaller
+    while (x->parent != y->parent) {
+      x = x->parent;
+      y = y->parent;
+    }
+    return x->key[0] < y->key[0];
+  }
+  struct Later {                              // heap order: the top is the next victim
+    bool operator()(const Node* a, const Node* b) const {
+      if (a->last_access != b->last_access) return a->last_access > b->last_access;
+      return path_less(b, a);
+    }
+  };
+  static bool host_victim(const Node* n) {
+    return n->mark == 0 && !n->host.empty() && n->dev.empty() && n->ref == 0 && n->children.empty();
+  }
+  static bool dev_victim(const Node* n) {
+    if (n->mark != 0 || n->dev.empty() || n->ref != 0) return false;
+    for (auto& kv : n->children)
+      if (!kv.second->dev.empty()) return false;
+    return true;
+  }
+  // Candidates are collected once per call; evicting a node can only make its parent a candidate,
+  // so the heap yields the same sequence as re-scanning the tree before every eviction.
   template <class Pred>
-  Node* lru(Pred&& pred) const {
-    Node* best = nullptr;
-    std::vector<int32_t> pb, pc;
-    for_each_node([&](const Node* cn) {
-      if (!pred(cn)) return;
-      Node* c = const_cast<Node*>(cn);
-      if (!best || c->last_access < best->last_access) {
-        best = c;
-        pb.clear();
-      } else if (c->last_access == best->last_access) {
-        if (pb.empty()) path_of(best, pb);
-        path_of(c, pc);
-        if (std::lexicographical_compare(pc.begin(), pc.end(), pb.begin(), pb.end())) {
-          best = c;
-          pb.swap(pc);
-        }
-      }
+  std::vector<Node*> victims(Pred&& pred) const {
+    std::vector<Node*> h;
+    for_each_node([&](const Node* n) {
+      if (pred(n)) h.push_back(const_cast<Node*>(n));
     });
-    return best;
+    std::make_heap(h.begin(), h.end(), Later{});
+    return h;
+  }
+  static Node* pop_victim(std::vector<Node*>& h) {
+    std::pop_heap(h.begin(), h.end(), Later{});
+    Node* v = h.back();
+    h.pop_back();
+    return v;
+  }
+  static void push_victim(std::vector<Node*>& h, Node* n) {
+    h.push_back(n);
+    std::push_heap(h.begin(), h.end(), Later{});
   }
 
   bool ensure_host(int64_t units) {
+    if (hpool.nfree() >= units) return true;
+    std::vector<Node*> h = victims(host_victim);
     while (hpool.nfree() < units) {
-      Node* v = lru([](const Node* n) {
-        return n->mark == 0 && !n->host.empty() && n->dev.empty() && n->ref == 0 && n->children.empty();
-      });
-      if (!v) return false;
+      if (h.empty()) return false;
+      Node* v = pop_victim(h);
+      if (!host_victim(v)) continue;
+      Node* parent = v->parent;
       for (int64_t s : v->host) hpool.release(s);
       remove_leaf(v);
+      if (parent != root && host_victim(parent)) push_victim(h, parent);
     }
     return true;
   }
 
   bool ensure_dev(int64_t units) {
+    if (dpool.nfree() >= units) return true;
+    std::vector<Node*> h = victims(dev_victim);
     while (dpool.nfree() < units) {
-      Node* v = lru([](const Node* n) {
-        if (n->mark != 0 || n->dev.empty() || n->ref != 0) return false;
-        for (auto& kv : n->children)
-          if (!kv.second->dev.empty()) return false;
-        return true;
-      });
-      if (!v) return false;
+      if (h.empty()) return false;
+      Node* v = pop_victim(h);
+      if (!dev_victim(v)) continue;
       if (v->host.empty()) {        // inclusive write-back before the drop
         if (!ensure_host(ceil_div(static_cast<int64_t>(v->key.size()), C))) return false;
         hpool.alloc(static_cast<int64_t>(v->key.size()), v->host);
@@ -294,6 +333,7 @@ struct strata_ctl {
       }
       for (int64_t s : v->dev) dpool.release(s);
       v->dev.clear();
+      if (v->parent != root && dev_victim(v->parent)) push_victim(h, v->parent);
     }
     return true;
   }
@@ -356,10 +396,26 @@ struct strata_ctl {
                                   int64_t* load_out, int64_t* comp_out) const {
     std::vector<int64_t> B;
     int64_t load = 0, comp = 0;
+    // overlap(r) = max over members b of host_overlap(r, b), kept incrementally: updated for every
+    // candidate when a member joins (only candidates with host tokens can overlap)
+    std::unordered_map<int64_t, int64_t> ov;
+    ov.reserve(Q.size() * 2);
     auto overlap = [&](int64_t r) {
-      int64_t o = 0;
-      for (int64_t b : B) o = std::max(o, host_overlap(st[r], st[b]));
-      return o;
+      auto it = ov.find(r);
+      return it == ov.end() ? int64_t(0) : it->second;
+    };
+    std::vector<int64_t> all = Q;                // every candidate (queue and, later, the D list)
+    std::unordered_map<int64_t, bool> in_b;
+    auto joined = [&](int64_t b) {
+      in_b[b] = true;
+      for (int64_t r : all)
+        if (!in_b.count(r) && st[r].host > 0) {
+          const int64_t o = host_overlap(st[r], st[b]);
+          if (o > 0) {
+            int64_t& cur = ov[r];
+            cur = std::max(cur, o);
+          }
+        }
     };
     auto eff_load = [&](int64_t r) { return st[r].host - overlap(r); };
     auto is_full = [&] { return (max_reqs > 0 && static_cast<int64_t>(B.size()) >= max_reqs) ||
@@ -378,6 +434,7 @@ struct strata_ctl {
       load += eff_load(r);
       comp += st[r].compute;
       B.push_back(r);
+      joined(r);
     };
     auto add_bundle_hit = [&] {                  // procedure AddBundleHit(Q, B)
       if (!bundle) return;
