@@ -16,6 +16,7 @@
 
 #include "strata.h"
 #include "strata_disk.h"
+#include "strata_ctl.h"
 
 static int failures = 0;
 #define EXPECT(cond, ...)                      \
@@ -52,6 +53,48 @@ static void cpu_checks(void) {
   strata_disk_t disk = (strata_disk_t)0x1;
   EXPECT(strata_disk_open(NULL, &disk) == STRATA_ERR_INVALID_ARG && disk == NULL, "disk NULL desc");
   EXPECT(strata_version() >= 100, "version");
+}
+
+/* The control plane (strata_ctl.h) is host code: a context offloaded earlier hits in the host tier,
+ * the scheduler dispatches the request, and its LOAD plan, decoded with strata.h's token formula,
+ * moves exactly the context's host slots to the request's device slots. */
+static void ctl_checks(void) {
+  strata_ctl_desc cd;
+  memset(&cd, 0, sizeof cd);
+  cd.page_size = 4; cd.chunk_tokens = 8; cd.num_pages = 64; cd.num_chunks = 16;
+  cd.deferral_threshold = 100; cd.loading_bound_ratio = 100.0;
+  strata_ctl_t c = NULL;
+  EXPECT(strata_ctl_create(NULL, &c) == STRATA_ERR_INVALID_ARG, "ctl NULL desc");
+  EXPECT(strata_ctl_create(&cd, &c) == STRATA_OK && c, "ctl create: %s", strata_last_error());
+  if (!c) return;
+  int32_t ctx[20], req[23];
+  int64_t hslots[20], dslots[23], n = 0;
+  for (int i = 0; i < 20; ++i) ctx[i] = req[i] = 1000 + i;
+  req[20] = 7; req[21] = 8; req[22] = 9;
+  EXPECT(strata_ctl_insert(c, ctx, 20, STRATA_TIER_HOST, 0.0, hslots) == STRATA_OK, "insert");
+  EXPECT(strata_ctl_submit(c, 42, req, 23) == STRATA_OK, "submit");
+  EXPECT(strata_ctl_submit(c, 42, req, 23) == STRATA_ERR_DUPLICATE, "duplicate id");
+  strata_ctl_round r;
+  EXPECT(strata_ctl_schedule(c, 1.0, &r) == STRATA_OK && r.num_batch == 1 && r.load_tokens == 20 &&
+         r.new_tokens == 3, "schedule: batch %lld load %lld new %lld", (long long)r.num_batch,
+         (long long)r.load_tokens, (long long)r.new_tokens);
+  EXPECT(strata_ctl_req_slots(c, 42, dslots, &n) == STRATA_OK && n == 23, "req slots");
+  strata_ctl_plan pl;
+  EXPECT(strata_ctl_plan_get(c, STRATA_CTL_LOAD, &pl) == STRATA_OK, "plan");
+  int64_t t = 0;
+  for (int64_t q = 0; q < pl.num_reqs; ++q)
+    for (int64_t i = 0; i < pl.num_tokens[q]; ++i, ++t) {
+      const int64_t ci = pl.chunk_offset[q] + i, pi = pl.page_offset[q] + i;
+      const int64_t h = (int64_t)pl.host_chunks[pl.chunk_start[q] + ci / 8] * 8 + ci % 8;
+      const int64_t dv = (int64_t)pl.dev_pages[pl.page_start[q] + pi / 4] * 4 + pi % 4;
+      EXPECT(t < 20 && h == hslots[t] && dv == dslots[t], "plan token %lld", (long long)t);
+    }
+  EXPECT(t == 20, "plan covers %lld tokens", (long long)t);
+  EXPECT(strata_ctl_complete(c, 42, 2.0) == STRATA_OK, "complete");
+  strata_ctl_match_t m;
+  EXPECT(strata_ctl_match(c, req, 23, &m) == STRATA_OK && m.device == 23 && m.total == 23, "match");
+  EXPECT(strata_ctl_bubble_steps(20.0, 5.0, 3.0, 8) == 5, "bubble steps");
+  EXPECT(strata_ctl_destroy(c) == STRATA_OK, "destroy");
 }
 
 typedef int (*malloc_fn)(void**, size_t);
@@ -118,6 +161,7 @@ static int gpu_checks(void) {
 
 int main(int argc, char** argv) {
   cpu_checks();
+  ctl_checks();
   if (argc > 1 && strcmp(argv[1], "gpu") == 0) gpu_checks();
   if (failures) {
     fprintf(stderr, "%d failure(s)\n", failures);
