@@ -89,3 +89,53 @@ def test_head_slice_partition():
         assert seen == list(range(H))
     with pytest.raises(ValueError):
         kvgen.head_slice(0, 3, 8)
+
+
+def _ctl_worker(rank, world, port, out_q):
+    """Every TP rank runs its own native control plane on the same request stream; its plans index
+    the same pages and chunks of its head slice, so they must be identical without any collective
+    on the data path.  Ranks compare digests of every round with all_gather."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import hashlib
+
+        from kvgen import traces
+        from paper_2508_18572_b200 import ctl as ctl_mod
+        rng = np.random.default_rng(7)             # the request stream every rank receives
+        fam = traces.random_prefix_family(rng, 200, 120, vocab=4, branch=0.8)
+        c = ctl_mod.Ctl(4, 16, 300, 200, threshold=20, ratio=4.0, max_batch_reqs=4, max_batch_tokens=500)
+        same = True
+        rid, t = 0, 0.0
+        for rnd in range(40):
+            for _ in range(3):
+                c.submit(rid, fam[(rid * 7) % len(fam)] + [rid % 4, (rid // 4) % 4])
+                rid += 1
+            out = c.schedule(t)
+            h = hashlib.sha256(repr((out, c.plan("load"), c.plan("writeback"))).encode()).digest()
+            mine = torch.frombuffer(bytearray(h), dtype=torch.uint8)
+            parts = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(parts, mine)
+            same &= all(torch.equal(p, parts[0]) for p in parts)
+            for r in out["batch"]:
+                c.complete(r, t + 0.5)
+            t += 1.0
+        if rank == 0:
+            out_q.put(bool(same))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_control_plane_identical_across_tp_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ctl_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    assert q.get(timeout=10), "TP ranks' control planes diverged"
