@@ -353,7 +353,11 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     if (e != cudaSuccess) return op_fail(e, "fused transfer kernel launch");
     ++p->counters.kernel_launches;
     cudaStream_t side = p->side[slot];
-    for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
+    // the last layer completes with the kernel: its event goes on the caller's stream, sparing the
+    // op's completion the side stream's flag-poll latency
+    e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + x->layer_end], s);
+    if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
+    for (int32_t l = x->layer_begin; l + 1 < x->layer_end; ++l) {
       if (g_wait_value32(reinterpret_cast<CUstream>(side), reinterpret_cast<CUdeviceptr>(fp.flags + l), fp.epoch,
                          CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
         return op_fail(cudaErrorUnknown, "cuStreamWaitValue32");

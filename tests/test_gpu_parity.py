@@ -180,6 +180,33 @@ def test_dma_engine_multi_piece(direction, group):
         c.close()
 
 
+@pytest.mark.parametrize("edge,ordered", [("1", "0"), ("1", "1"), ("4", "1"), ("16", "0")])
+@pytest.mark.parametrize("direction", ["load", "offload"])
+def test_dma_engine_piece_schedule(direction, edge, ordered, monkeypatch):
+    """The DMA engine's piece schedule (edge pieces of the first / last layer, the per-piece copy
+    barrier) changes only timing: the result stays the oracle's and layer events stay ordered."""
+    monkeypatch.setenv("STRATA_DMA_EDGE_SPLIT", edge)
+    monkeypatch.setenv("STRATA_DMA_ORDERED", ordered)
+    g = Geometry(4, 8, 128, 2, 1, 64, 40960, 560)
+    rng = kvgen.rng_for(22)
+    q = kvgen.make_requests(rng, [21000, 12000, 300], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
+    c = GpuCase(g, q, dev_fill="canary" if direction == "load" else "random")
+    try:
+        if direction == "load":
+            t = c.pool.load(c.reqs, 0, 4, engine=st.STRATA_ENGINE_DMA)
+            _sync()
+            c.check_load(0, 4)
+            done = [c.pool.layer_elapsed_ms(t, l) for l in range(0, 4)]
+            assert all(b >= a for a, b in zip(done, done[1:])), done
+        else:
+            before = c.pool.host.copy()
+            c.pool.offload(c.reqs, 0, 4, engine=st.STRATA_ENGINE_DMA)
+            _sync()
+            assert np.array_equal(c.pool.host, c.expected_offload(before, 0, 4))
+    finally:
+        c.close()
+
+
 def test_dma_engine_needs_host_list():
     g = kvgen.geometry("tiny")
     q = kvgen.make_requests(kvgen.rng_for(0), [64], g.P, g.C, g.num_pages, g.num_chunks)
