@@ -43,6 +43,7 @@ class Geometry:
     C: int
     num_pages: int
     num_chunks: int
+    kv: int = 2   # KV buffers per layer: 2 (K and V: MHA/GQA), 1 (MLA's shared latent, R27)
 
     @property
     def token_bytes(self) -> int:
@@ -51,8 +52,8 @@ class Geometry:
 
     @property
     def chunk_bytes(self) -> int:
-        """One host chunk holds C tokens of every layer's K and V: L*2*C*S_tok bytes."""
-        return self.L * 2 * self.C * self.token_bytes
+        """One host chunk holds C tokens of every layer's K and V: L*kv*C*S_tok bytes."""
+        return self.L * self.kv * self.C * self.token_bytes
 
     @property
     def host_bytes(self) -> int:
@@ -77,6 +78,11 @@ CONFIGS: Dict[str, dict] = {
     # Llama-3.1-70B: 8 KV heads, TP=8 -> 1 head per GPU (per-rank geometry).
     "llama70b_tp8": dict(L=80, H=1, D=128, e=2, P=1, C=64, n=[131072], num_pages=163840,
                          num_chunks=2560, tp=8),
+    # DeepSeek-V3 MLA latent cache (one buffer per layer: kv_lora_rank 512 + rope 64 = 576 bf16 per
+    # token; 61 layers), 32K-token prefix.  A variant beyond BASELINE.json's configs;
+    # the latent is replicated, not head-sharded, under TP, so multi-GPU runs are replicas.
+    "deepseek_v3_mla": dict(L=61, H=1, D=576, e=2, P=1, C=64, n=[32768], num_pages=40960,
+                            num_chunks=640, tp=1, kv=1),
 }
 
 
@@ -89,7 +95,7 @@ def geometry(name: str, P: Optional[int] = None, **over) -> Geometry:
         c["num_pages"] = -(-slots // P)
         c["P"] = P
     return Geometry(L=c["L"], H=c["H"], D=c["D"], e=c["e"], P=c["P"], C=c["C"],
-                    num_pages=c["num_pages"], num_chunks=c["num_chunks"])
+                    num_pages=c["num_pages"], num_chunks=c["num_chunks"], kv=c.get("kv", 2))
 
 
 def rng_for(seed: int) -> np.random.Generator:

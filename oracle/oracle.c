@@ -7,15 +7,18 @@
  *
  * What it computes (the plain definition; a copy, not an approximation — DESIGN.md §3):
  *
- *   LOAD:    for r, for i in [0,n_r), for l in [l0,l1), for kv in {K,V}, for h in [0,H):
+ *   LOAD:    for r, for i in [0,n_r), for l in [l0,l1), for kv in [0,KV), for h in [0,H):
  *              dev'[dst(r,i,l,kv,h) : +D*e] = host[src(r,i,l,kv,h) : +D*e]
  *            every other device byte is unchanged.
  *   OFFLOAD: the same loops with source and destination swapped; every other host byte unchanged.
  *
  *   ci = off_c[r] + i;  hc = host_chunks[chunk_start[r] + ci / C];  ho = ci % C
  *   pi = off_p[r] + i;  pg = dev_pages [page_start [r] + pi / P];  po = pi % P
- *   src(l,kv,h) = host + hc*chunk_bytes + ((l*2 + kv)*C + ho)*H*D*e + h*D*e
+ *   src(l,kv,h) = host + hc*chunk_bytes + ((l*KV + kv)*C + ho)*H*D*e + h*D*e,  chunk_bytes = L*KV*C*H*D*e
  *   dst(l,kv,h) = pool[l][kv] + pg*page_stride + po*token_stride + h*head_stride
+ *
+ *   KV = 2 (a K and a V buffer per layer, MHA/GQA) or KV = 1 (one buffer per layer: MLA's latent
+ *   cache, where K and V are both derived from one compressed vector per token — DESIGN.md R27).
  *
  * Passages followed:
  *   - GPU-assisted I/O moves KV between "CPU registered pinned memory" and GPU global memory
@@ -47,6 +50,7 @@ typedef struct {
     int64_t head_stride;       /* device bytes between heads of a token */
     int64_t num_pages;         /* device capacity in pages */
     int64_t num_chunks;        /* host capacity in chunks */
+    int64_t KV;                /* buffers per layer: 2 (K, V) or 1 (MLA latent) */
 } oracle_geom;
 
 typedef struct {
@@ -66,7 +70,7 @@ static int oracle_move(const oracle_geom* g, uint8_t* host, uint8_t* const* k_im
                        uint8_t* const* v_img, const oracle_reqs* q, int dir, int nthreads) {
     const int64_t row_bytes = g->D * g->e;            /* one head of one token */
     const int64_t tok_bytes = g->H * g->D * g->e;      /* S_tok */
-    const int64_t chunk_bytes = g->L * 2 * g->C * tok_bytes;
+    const int64_t chunk_bytes = g->L * g->KV * g->C * tok_bytes;
     int bad = 0;
     (void)nthreads;
     for (int64_t r = 0; r < q->R; ++r) {
@@ -88,10 +92,10 @@ static int oracle_move(const oracle_geom* g, uint8_t* host, uint8_t* const* k_im
                 continue;
             }
             for (int64_t l = q->layer_begin; l < q->layer_end; ++l) {
-                for (int64_t kv = 0; kv < 2; ++kv) {
+                for (int64_t kv = 0; kv < g->KV; ++kv) {
                     uint8_t* pool = kv == 0 ? k_img[l] : v_img[l];
                     for (int64_t h = 0; h < g->H; ++h) {
-                        uint8_t* hp = host + hc * chunk_bytes + ((l * 2 + kv) * g->C + ho) * tok_bytes +
+                        uint8_t* hp = host + hc * chunk_bytes + ((l * g->KV + kv) * g->C + ho) * tok_bytes +
                                       h * row_bytes;
                         uint8_t* dp = pool + pg * g->page_stride + po * g->token_stride +
                                       h * g->head_stride;

@@ -3,7 +3,8 @@
 It computes the same plain definition as ``oracle.c`` but by a different route:
 instead of a per-(token, layer, kv, head) memcpy loop it views
 
-    host  as  [num_chunks, L, 2, C, H, D*e]               (page-first host chunk)
+    host  as  [num_chunks, L, KV, C, H, D*e]              (page-first host chunk, PAPER.md:286, :290;
+                                                            KV = 2 for K,V or 1 for an MLA latent)
     pool  as  [num_pages, P, H, D*e] with the byte strides  (layer-first paged pool, PAPER.md:284,
                                                             :653-655)
 
@@ -20,7 +21,11 @@ from numpy.lib.stride_tricks import as_strided
 
 def _host_view(host: np.ndarray, g) -> np.ndarray:
     # [num_chunks][L][K,V][C][H][D*e]: "arranges layers of a page contiguously"
-    return host.reshape(g.num_chunks, g.L, 2, g.C, g.H, g.D * g.e)
+    return host.reshape(g.num_chunks, g.L, _kv(g), g.C, g.H, g.D * g.e)
+
+
+def _kv(g) -> int:
+    return getattr(g, "kv", 2)
 
 
 def _pool_view(buf: np.ndarray, g, strides) -> np.ndarray:
@@ -57,7 +62,7 @@ def load(g, host: np.ndarray, k_imgs: Sequence[np.ndarray], v_imgs: Sequence[np.
         hc, ho, pg, po = _token_coords(q, r, g)
         _check(g, hc, pg)
         for l in range(layer_begin, layer_end):
-            for kv, imgs in ((0, k_imgs), (1, v_imgs)):
+            for kv, imgs in ((0, k_imgs), (1, v_imgs))[:_kv(g)]:
                 dev = _pool_view(imgs[l], g, strides)
                 dev[pg, po] = hv[hc, l, kv, ho]
 
@@ -71,7 +76,7 @@ def offload(g, host: np.ndarray, k_imgs: Sequence[np.ndarray], v_imgs: Sequence[
         hc, ho, pg, po = _token_coords(q, r, g)
         _check(g, hc, pg)
         for l in range(layer_begin, layer_end):
-            for kv, imgs in ((0, k_imgs), (1, v_imgs)):
+            for kv, imgs in ((0, k_imgs), (1, v_imgs))[:_kv(g)]:
                 dev = _pool_view(imgs[l], g, strides)
                 hv[hc, l, kv, ho] = dev[pg, po]
 

@@ -40,10 +40,10 @@ def dev_images(g, fill=CANARY, rng=None, strides=None):
 def tagged_host(g) -> np.ndarray:
     """Host pool where every 16-byte vector encodes its own coordinates as 4 x u32:
     (chunk, (layer<<1)|kv, token_in_chunk, (head<<16)|vec)  with vec < D*e/16.
-    Layout: [num_chunks][L][2][C][H][D*e/16] vectors (reading R1)."""
+    Layout: [num_chunks][L][KV][C][H][D*e/16] vectors (reading R1; KV = g.kv, 2 or 1 for MLA)."""
     vph = g.D * g.e // 16
     assert vph >= 1 and g.D * g.e % 16 == 0
-    shape = (g.num_chunks, g.L, 2, g.C, g.H, vph)
+    shape = (g.num_chunks, g.L, getattr(g, "kv", 2), g.C, g.H, vph)
     c, l, kv, t, h, v = np.meshgrid(*[np.arange(s, dtype=np.uint32) for s in shape], indexing="ij")
     tags = np.stack([c, (l << 1) | kv, t, (h << 16) | v], axis=-1)
     return np.ascontiguousarray(tags).view(np.uint8).reshape(-1)
