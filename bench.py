@@ -146,7 +146,7 @@ def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 12.0):
     for a in k + v:
         a.fill(0)   # fault the pages in outside the timed region
     threads = oracle.max_threads()
-    bytes_per = 2 * g.L * q.total_tokens * g.token_bytes
+    bytes_per = g.kv * g.L * q.total_tokens * g.token_bytes
     times = []
     t_start = time.time()
     while not times or (time.time() - t_start < budget_s and len(times) < 5):
@@ -173,7 +173,7 @@ def run_reference(args):
     k = [np.zeros(nb, np.uint8) for _ in range(g.L)]
     v = [np.zeros(nb, np.uint8) for _ in range(g.L)]
     threads = oracle.max_threads()
-    bytes_per = 2 * g.L * q.total_tokens * g.token_bytes
+    bytes_per = g.kv * g.L * q.total_tokens * g.token_bytes
     for _ in range(args.warmup):
         oracle.load(g, host, k, v, q, 0, g.L, nthreads=threads)
     t0 = time.perf_counter()
@@ -195,9 +195,11 @@ def run_reference(args):
 
 def _config(args, g, q):
     return {"workload": args.config, "layers": g.L, "kv_heads_per_gpu": g.H, "head_dim": g.D, "kv_dtype": "bf16",
+            "kv_buffers_per_layer": g.kv,
             "page_size": g.P, "host_chunk_tokens": g.C, "tokens_per_gpu": q.total_tokens,
-            "requests": q.R, "fragmentation": args.frag, "bytes_per_step_per_gpu": 2 * g.L * q.total_tokens * g.token_bytes,
-            "l2": "no flush: each step moves 4+ GiB, far above the 126 MB L2", "parallelism": f"replicas x{args.gpus}"}
+            "requests": q.R, "fragmentation": args.frag, "bytes_per_step_per_gpu": g.kv * g.L * q.total_tokens * g.token_bytes,
+            "l2": f"no flush: each step moves {g.kv * g.L * q.total_tokens * g.token_bytes / 2**30:.1f} GiB, "
+                  "far above the 126 MB L2", "parallelism": f"replicas x{args.gpus}"}
 
 
 def main():
@@ -228,12 +230,13 @@ def main():
     g, q = workload(args, rank, world)
     nb = g.num_pages * g.P * g.token_bytes
     k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
-    v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)] if g.kv == 2 else k
     pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
-                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks, device=local)
+                       k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=g.num_pages,
+                       num_chunks=g.num_chunks, device=local)
     kvgen.fill_random(pool.host, args.seed * 1000 + rank)
     reqs = st.Requests.from_kvgen(q, device=local)
-    bytes_step = 2 * g.L * q.total_tokens * g.token_bytes
+    bytes_step = g.kv * g.L * q.total_tokens * g.token_bytes
     io = torch.cuda.Stream()
 
     def step():

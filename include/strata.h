@@ -16,11 +16,15 @@
  * LAYOUTS (DESIGN.md §3 readings R1-R5)
  *   Host tier, page-first ("arranges layers of a page contiguously"):
  *     num_chunks chunks of C tokens; chunk = [L][K,V][C][H][D] elements of e bytes,
- *     chunk_bytes = L*2*C*H*D*e.  Token ho of chunk hc, layer l, kv, head h starts at
- *       host_base + hc*chunk_bytes + ((l*2 + kv)*C + ho)*H*D*e + h*D*e.
+ *     chunk_bytes = L*KV*C*H*D*e.  Token ho of chunk hc, layer l, kv, head h starts at
+ *       host_base + hc*chunk_bytes + ((l*KV + kv)*C + ho)*H*D*e + h*D*e.
+ *     KV = 2 (a K and a V buffer per layer), or KV = 1 with STRATA_POOL_SINGLE_KV (R27).
  *   Device pool, layer-first, paged: one K and one V buffer per layer,
  *     caller-owned; token slot (page pg, offset po < P), head h starts at
  *       {k,v}_ptrs[l] + pg*page_stride + po*token_stride + h*head_stride.
+ *     With STRATA_POOL_SINGLE_KV a layer has one buffer (k_ptrs; v_ptrs unused, may be NULL):
+ *     MLA's latent cache (DeepSeek-V2/V3: one compressed vector per token from which K and V are
+ *     both derived, e.g. H = 1, D = 576, bf16 -> 1152 B per token and layer).
  *     Default strides (0) are NHD: token_stride = H*D*e, head_stride = D*e, page_stride = P*H*D*e.
  *   Request r moves num_tokens[r] tokens; token i (0-based in this call) lives at
  *       host:   ci = chunk_offset[r] + i, chunk host_chunks[chunk_start[r] + ci / C], position ci % C
@@ -76,8 +80,10 @@ enum strata_pool_flags {
   STRATA_HOST_WRITECOMBINED = 2, /* library-allocated host tier via cudaHostAllocWriteCombined */
   STRATA_VALIDATE = 4,           /* check index lists on the device before every transfer */
   STRATA_HOST_NO_NUMA_BIND = 8,  /* do not bind library-allocated host memory to the GPU's node */
-  STRATA_HOST_CUDA_ALLOC = 16    /* library-allocated host tier via cudaHostAlloc(Mapped|Portable)
+  STRATA_HOST_CUDA_ALLOC = 16,   /* library-allocated host tier via cudaHostAlloc(Mapped|Portable)
                                     instead of mmap + cudaHostRegister */
+  STRATA_POOL_SINGLE_KV = 32     /* one KV buffer per layer (MLA latent cache, KV = 1 in LAYOUTS);
+                                    v_ptrs is ignored */
 };
 
 /* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
@@ -105,7 +111,8 @@ typedef struct {
   int32_t chunk_tokens;           /* C >= 1: host tokens per chunk */
   int32_t flags;                  /* strata_pool_flags */
   void* const* k_ptrs;            /* [num_layers] device base of each layer's K buffer (copied) */
-  void* const* v_ptrs;            /* [num_layers] device base of each layer's V buffer (copied) */
+  void* const* v_ptrs;            /* [num_layers] device base of each layer's V buffer (copied);
+                                     NULL allowed with STRATA_POOL_SINGLE_KV */
   int64_t page_stride;            /* device bytes between pages   (0 = P*H*D*e) */
   int64_t token_stride;           /* device bytes between tokens  (0 = H*D*e) */
   int64_t head_stride;            /* device bytes between heads   (0 = D*e) */

@@ -22,7 +22,7 @@ import numpy as np
 from . import _lib
 from ._lib import (STRATA_D2H, STRATA_ENGINE_DEFAULT, STRATA_ENGINE_LDG, STRATA_ENGINE_TMA,  # noqa: F401
                    STRATA_ENGINE_TMA_BULK, STRATA_ENGINE_DMA,
-                   STRATA_H2D, STRATA_HOST_HUGEPAGES, STRATA_HOST_NO_NUMA_BIND,
+                   STRATA_H2D, STRATA_HOST_HUGEPAGES, STRATA_HOST_NO_NUMA_BIND, STRATA_POOL_SINGLE_KV,
                    STRATA_HOST_WRITECOMBINED, STRATA_VALIDATE, PoolDesc, StrataError, Xfer, check)
 
 __all__ = [
@@ -189,11 +189,15 @@ class HostPool:
     """
 
     def __init__(self, *, num_layers: int, num_heads: int, head_dim: int, elem_bytes: int, page_size: int,
-                 chunk_tokens: int, k_ptrs: Sequence, v_ptrs: Sequence, num_pages: int, num_chunks: int,
+                 chunk_tokens: int, k_ptrs: Sequence, v_ptrs: Optional[Sequence], num_pages: int, num_chunks: int,
                  device: int = 0, flags: int = 0, host: Optional[np.ndarray] = None,
                  strides=(0, 0, 0)):
         def ptr(x):
             return int(x) if isinstance(x, int) else int(x.data_ptr())
+        # v_ptrs=None: one buffer per layer (MLA latent cache, STRATA_POOL_SINGLE_KV)
+        if v_ptrs is None:
+            flags |= STRATA_POOL_SINGLE_KV
+            v_ptrs = k_ptrs
         self._k = (ctypes.c_void_p * num_layers)(*[ptr(x) for x in k_ptrs])
         self._v = (ctypes.c_void_p * num_layers)(*[ptr(x) for x in v_ptrs])
         self._host_owner = host

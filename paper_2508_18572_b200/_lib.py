@@ -31,6 +31,7 @@ STRATA_HOST_WRITECOMBINED = 2
 STRATA_VALIDATE = 4
 STRATA_HOST_NO_NUMA_BIND = 8
 STRATA_HOST_CUDA_ALLOC = 16
+STRATA_POOL_SINGLE_KV = 32
 
 STRATA_ENGINE_DEFAULT = 0
 STRATA_ENGINE_LDG = 1

@@ -95,7 +95,9 @@ int check_desc(const strata_pool_desc* d) {
     return fail(STRATA_ERR_INVALID_ARG, "num_pages and num_chunks must be >= 1");
   if (d->num_pages > INT32_MAX || d->num_chunks > INT32_MAX)
     return fail(STRATA_ERR_INVALID_ARG, "pool indices are int32 (R10): num_pages/num_chunks < 2^31");
-  if (!d->k_ptrs || !d->v_ptrs) return fail(STRATA_ERR_INVALID_ARG, "k_ptrs / v_ptrs is NULL");
+  const bool single = d->flags & STRATA_POOL_SINGLE_KV;
+  const int64_t nkv = single ? 1 : 2;
+  if (!d->k_ptrs || (!single && !d->v_ptrs)) return fail(STRATA_ERR_INVALID_ARG, "k_ptrs / v_ptrs is NULL");
   const int64_t head_bytes = int64_t(d->head_dim) * d->elem_bytes;
   const int64_t tok = head_bytes * d->num_heads;
   if (tok % 16) return fail(STRATA_ERR_ALIGNMENT, "H*D*e = %lld is not a multiple of 16 (R12)", (long long)tok);
@@ -110,13 +112,14 @@ int check_desc(const strata_pool_desc* d) {
   if (hs != head_bytes && head_bytes % 16)
     return fail(STRATA_ERR_ALIGNMENT, "non-contiguous heads need D*e %% 16 == 0");
   for (int l = 0; l < d->num_layers; ++l) {
-    if (!d->k_ptrs[l] || !d->v_ptrs[l]) return fail(STRATA_ERR_INVALID_ARG, "layer %d K/V pointer is NULL", l);
-    if (!aligned16(d->k_ptrs[l]) || !aligned16(d->v_ptrs[l]))
+    void* const vp = single ? d->k_ptrs[l] : d->v_ptrs[l];
+    if (!d->k_ptrs[l] || !vp) return fail(STRATA_ERR_INVALID_ARG, "layer %d K/V pointer is NULL", l);
+    if (!aligned16(d->k_ptrs[l]) || !aligned16(vp))
       return fail(STRATA_ERR_ALIGNMENT, "layer %d K/V pointer not 16-byte aligned", l);
   }
   if (d->host_base && !aligned16(d->host_base)) return fail(STRATA_ERR_ALIGNMENT, "host_base not 16-byte aligned");
-  const int64_t chunk = int64_t(d->num_layers) * 2 * d->chunk_tokens * tok;
-  if (chunk / tok / 2 / d->chunk_tokens != d->num_layers || d->num_chunks > INT64_MAX / chunk)
+  const int64_t chunk = int64_t(d->num_layers) * nkv * d->chunk_tokens * tok;
+  if (chunk / tok / nkv / d->chunk_tokens != d->num_layers || d->num_chunks > INT64_MAX / chunk)
     return fail(STRATA_ERR_INVALID_ARG, "host tier size overflows");
   return STRATA_OK;
 }
@@ -161,13 +164,16 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
   strata_pool* p = new (std::nothrow) strata_pool();
   if (!p) return fail(STRATA_ERR_OOM, "out of host memory");
   p->d = *d;
+  p->nkv = (d->flags & STRATA_POOL_SINGLE_KV) ? 1 : 2;
   p->k.assign(d->k_ptrs, d->k_ptrs + d->num_layers);
-  p->v.assign(d->v_ptrs, d->v_ptrs + d->num_layers);
+  // a single-buffer pool never touches its V bases; they alias K so no path sees a null pointer
+  if (p->nkv == 2) p->v.assign(d->v_ptrs, d->v_ptrs + d->num_layers);
+  else p->v = p->k;
   p->d.k_ptrs = p->k.data();
   p->d.v_ptrs = p->v.data();
   p->head_bytes = int64_t(d->head_dim) * d->elem_bytes;
   p->tok_bytes = p->head_bytes * d->num_heads;
-  p->chunk_bytes = int64_t(d->num_layers) * 2 * d->chunk_tokens * p->tok_bytes;
+  p->chunk_bytes = int64_t(d->num_layers) * p->nkv * d->chunk_tokens * p->tok_bytes;
   p->token_stride = d->token_stride ? d->token_stride : p->tok_bytes;
   p->head_stride = d->head_stride ? d->head_stride : p->head_bytes;
   p->page_stride = d->page_stride ? d->page_stride : d->page_size * p->token_stride;

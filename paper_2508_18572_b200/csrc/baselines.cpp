@@ -48,7 +48,7 @@ int for_each_copy(strata_pool_t p, const strata_xfer* x, int dir, F&& emit) {
   const bool rows_contig = p->head_stride == p->head_bytes;
   const bool pages_contig = rows_contig && p->token_stride == tok;
   for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
-    for (int kv = 0; kv < 2; ++kv) {
+    for (int kv = 0; kv < p->nkv; ++kv) {
       char* base = static_cast<char*>(kv ? p->v[l] : p->k[l]);
       for (int32_t r = 0; r < x->num_reqs; ++r) {
         const int64_t n = x->num_tokens[r];
@@ -63,7 +63,7 @@ int for_each_copy(strata_pool_t p, const strata_xfer* x, int dir, F&& emit) {
             return bfail(STRATA_ERR_INDEX_RANGE, "index out of range");
           int64_t run = 1;
           if (pages_contig) run = std::min({n - i, C - ci % C, P - pi % P});
-          char* h = p->host + hc * p->chunk_bytes + ((int64_t(l) * 2 + kv) * C + ci % C) * tok;
+          char* h = p->host + hc * p->chunk_bytes + ((int64_t(l) * p->nkv + kv) * C + ci % C) * tok;
           char* d = base + pg * p->page_stride + (pi % P) * p->token_stride;
           if (rows_contig) {
             if (dir == 0) emit(Copy{d, h, size_t(run * tok)});

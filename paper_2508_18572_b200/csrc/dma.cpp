@@ -150,13 +150,14 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
       i += cnt;
     }
   }
-  const size_t unit = static_cast<size_t>(2 * C * tok);             // one chunk-layer: K rows, V rows
+  const int64_t nkv = p->nkv;
+  const size_t unit = static_cast<size_t>(nkv * C * tok);           // one chunk-layer: K rows, V rows
   // layers per copy run.  Loads keep per-layer granularity (grouping does not raise H2D throughput,
   // profiles/r01/sweep_groups*.jsonl); offloads ("backup", a non-critical path) group
   // layers until a run is >= 128 KiB, which D2H copies need (70B TP=8 rank: 44.6 -> 55.8 GB/s).
   int G = x->layer_group;
   if (G <= 0)
-    G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + 2 * C * tok - 1) / (2 * C * tok)));
+    G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + int64_t(unit) - 1) / int64_t(unit)));
   G = std::max(1, std::min(G, std::max(1, x->layer_end - x->layer_begin)));
   const size_t gunit = unit * static_cast<size_t>(G);                 // staging bytes per chunk
   size_t stage_target = kStageTarget;
@@ -227,7 +228,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
       for (size_t j = 0; j < pc.count; ++j) {
         const ChunkPos& cp = pos[pc.first + j];
         const int64_t hc = x->host_chunks_host[x->chunk_start[cp.req] + cp.cq];
-        char* h = p->host + hc * p->chunk_bytes + int64_t(lg) * 2 * C * tok;
+        char* h = p->host + hc * p->chunk_bytes + int64_t(lg) * int64_t(unit);
         char* d = stage + j * gunit;
         auto add = [&](int64_t off, int64_t bytes) {
           dst.push_back(dir == 0 ? d + off : h + off);
@@ -235,11 +236,11 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
           sz.push_back(static_cast<size_t>(bytes));
         };
         if (cp.lo == 0 && cp.cnt == C) {
-          add(0, gl * 2 * C * tok);                    // the group's K,V runs are adjacent: one copy
+          add(0, gl * int64_t(unit));                  // the group's K,V runs are adjacent: one copy
         } else {
           for (int g = 0; g < gl; ++g) {
-            add(g * 2 * C * tok + cp.lo * tok, cp.cnt * tok);        // K rows of layer lg+g
-            add(g * 2 * C * tok + (C + cp.lo) * tok, cp.cnt * tok);  // V rows
+            add(g * int64_t(unit) + cp.lo * tok, cp.cnt * tok);                     // K rows of layer lg+g
+            if (nkv == 2) add(g * int64_t(unit) + (C + cp.lo) * tok, cp.cnt * tok);  // V rows
           }
         }
       }
@@ -264,14 +265,14 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
       }
       xp.ntok = acc;
       xp.host = stage;
-      const int64_t groups = (2LL * acc + xp.rows_per_group - 1) / xp.rows_per_group;
+      const int64_t groups = (nkv * acc + xp.rows_per_group - 1) / xp.rows_per_group;
       const int c = static_cast<int>(std::min<int64_t>(ctas, (groups * 32 + threads - 1) / threads));
       // one scatter / gather launch per layer of the group over the slot's layer sub-blocks
       auto launch_group = [&](int kdir) -> cudaError_t {
         for (int g = 0; g < gl; ++g) {
           xp.kbase = static_cast<char*>(p->k[lg + g]);
           xp.vbase = static_cast<char*>(p->v[lg + g]);
-          xp.layer_off = int64_t(g) * 2 * C * tok;
+          xp.layer_off = int64_t(g) * int64_t(unit);
           cudaError_t le = strata::launch_ldg(xp, kdir, c, threads, unroll, s);
           if (le != cudaSuccess) return le;
           ++p->counters.kernel_launches;

@@ -37,14 +37,15 @@ struct XferParams {
   int32_t head_bytes;           // D*e
   int32_t vpt;                  // 16-byte vectors per token row = tok_bytes/16
   int32_t vpt_shift;            // log2(vpt) if vpt is a power of two, else -1
+  uint32_t vpt_magic;           // else: row = umulhi(idx, vpt_magic) exactly for idx < 32*vpt (0 = divide)
   int32_t vph;                  // 16-byte vectors per head = head_bytes/16
   int32_t rows_per_group;       // LDG engine: token rows handled by one warp iteration (<= 32)
   int32_t tma_rows;             // TMA engine: token rows per pipeline stage (<= 32)
   int32_t tma_stages;           // TMA engine: pipeline depth
   int32_t tma_stage_bytes;      // TMA engine: bytes per stage (>= tma_rows * tok_bytes)
   int32_t c_shift, p_shift;     // log2(C), log2(P) when powers of two, else -1
-  int64_t chunk_bytes;          // L*2*C*S_tok
-  int64_t layer_off;            // byte offset of (layer, K) inside a host chunk: l*2*C*S_tok
+  int64_t chunk_bytes;          // L*KV*C*S_tok
+  int64_t layer_off;            // byte offset of (layer, K) inside a host chunk: l*KV*C*S_tok
   int64_t kv_off;               // byte offset from K to V inside a chunk layer: C*S_tok
   int64_t page_stride, token_stride, head_stride;
   // data
@@ -54,7 +55,7 @@ struct XferParams {
   const int32_t* host_chunks;   // device index lists
   const int32_t* dev_pages;
   int32_t ntok;                 // tokens in this launch
-  int32_t pad_;
+  int32_t nkv;                  // KV buffers per layer: 2 (K, V) or 1 (MLA latent); rows = nkv*ntok
   ReqTable rt;
 };
 
@@ -107,6 +108,7 @@ struct strata_pool {
   strata_pool_desc d;                 // copy; k_ptrs/v_ptrs re-pointed at the vectors below
   std::vector<void*> k, v;
   int64_t tok_bytes, head_bytes, chunk_bytes;
+  int32_t nkv = 2;                    // KV buffers per layer (1: STRATA_POOL_SINGLE_KV)
   int64_t page_stride, token_stride, head_stride;
   // host tier
   char* host = nullptr;               // host address
@@ -194,6 +196,7 @@ constexpr int kTmaStageTarget = 32 << 10;
 int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan);                     // transfer.cpp
 void fill_table(const strata_xfer* x, const Plan& plan, const Batch& b, ReqTable& rt);        // transfer.cpp
 int ilog2_exact(int v);                                                                       // transfer.cpp
+uint32_t div_magic(int d, int n_max);   // m with umulhi(n, m) == n / d for n < n_max, or 0  transfer.cpp
 int transfer(strata_pool* p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir); // transfer.cpp
 int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, XferParams xp, cudaStream_t s,
                  int dir, int slot_ev);                                                       // dma.cpp

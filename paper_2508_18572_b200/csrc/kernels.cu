@@ -33,8 +33,8 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------------------------------------
 // Index fetch + layout transform for one token row.  Row = (kv, g): kv-major over the launch's
-// flat tokens (rows [0,N) are K, [N,2N) are V), so consecutive rows of one chunk are consecutive
-// host bytes.  Returns the host address and the device address of the row's first byte.
+// flat tokens (rows [0,N) are K, [N,2N) are V; a single-buffer pool has only [0,N)), so
+// consecutive rows of one chunk are consecutive host bytes.  Returns the host address and the device address of the row's first byte.
 __device__ __forceinline__ int find_req(const ReqTable& rt, int32_t g) {
   int lo = 0, hi = rt.n - 1;  // first r with tok_end[r] > g
   while (lo < hi) {
@@ -69,6 +69,13 @@ __device__ __forceinline__ RowIdx row_fetch(const XferParams& p, int64_t row) {
   x.hc = __ldg(p.host_chunks + p.rt.chunk_base[r] + cq);
   x.pg = __ldg(p.dev_pages + p.rt.page_base[r] + pq);
   return x;
+}
+
+// Row of 16-byte vector idx inside a group of rows (idx < 32 * vpt).
+__device__ __forceinline__ int vec_row(const XferParams& p, int idx) {
+  if (p.vpt_shift >= 0) return idx >> p.vpt_shift;
+  if (p.vpt_magic) return static_cast<int>(__umulhi(static_cast<unsigned>(idx), p.vpt_magic));
+  return idx / p.vpt;
 }
 
 __device__ __forceinline__ RowIdx row_none() {
@@ -112,7 +119,7 @@ __device__ __forceinline__ void st_vec(void* ptr, const int4& v) {
 template <int U, bool CONTIG, int DIR>
 __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char* vbase, int64_t layer_off,
                                           RowIdx nx, int64_t warp, int64_t nwarps, int lane) {
-  const int64_t nrows = 2LL * p.ntok;
+  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
   const int RG = p.rows_per_group;
   const int64_t ngroups = (nrows + RG - 1) / RG;
   // lane t fetches row t of the group; the next group's fetch is issued before this group's data
@@ -137,7 +144,7 @@ __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int idx = base + j * 32 + lane;
-        const int rl = p.vpt_shift >= 0 ? (idx >> p.vpt_shift) : (idx / p.vpt);
+        const int rl = vec_row(p, idx);
         const int w = idx - rl * p.vpt;
         const uint64_t s = __shfl_sync(kFull, my_src, rl & 31);
         if (idx < nvec) {
@@ -154,7 +161,7 @@ __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char
 #pragma unroll
       for (int j = 0; j < U; ++j) {
         const int idx = base + j * 32 + lane;
-        const int rl = p.vpt_shift >= 0 ? (idx >> p.vpt_shift) : (idx / p.vpt);
+        const int rl = vec_row(p, idx);
         const int w = idx - rl * p.vpt;
         const uint64_t d = __shfl_sync(kFull, my_dst, rl & 31);
         if (idx < nvec) {
@@ -173,7 +180,7 @@ __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char
 }
 
 __device__ __forceinline__ RowIdx ldg_first(const XferParams& p, int64_t warp, int lane) {
-  const int64_t nrows = 2LL * p.ntok;
+  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
   const int64_t ngroups = (nrows + p.rows_per_group - 1) / p.rows_per_group;
   const int64_t row = warp * p.rows_per_group + lane;
   return (warp < ngroups && lane < p.rows_per_group && row < nrows) ? row_fetch(p, row) : row_none();
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const RowIdx first = ldg_first(p, warp, lane);
-  const int64_t layer_step = 2LL * p.C * p.tok_bytes;
+  const int64_t layer_step = static_cast<int64_t>(p.nkv) * p.C * p.tok_bytes;
   for (int l = fp.l0; l < fp.l1; ++l) {
     ldg_layer<U, CONTIG, DIR>(p, fp.kb[l], fp.vb[l], int64_t(l) * layer_step, first, warp, nwarps, lane);
     __syncwarp();
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(32, 1) tma_kernel(const __grid_constant__ Xfer
   }
   __syncwarp();
 
-  const int64_t nrows = 2LL * p.ntok;
+  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
   const int64_t npieces = (nrows + T - 1) / T;
   const int64_t my = npieces > blockIdx.x ? (npieces - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel
   }
   __syncthreads();
 
-  const int64_t nrows = 2LL * p.ntok;
+  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
   const int64_t npieces = (nrows + T - 1) / T;
   const int64_t my = npieces > blockIdx.x ? (npieces - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -476,7 +483,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel
       const uint64_t* tab = tab_addr + s * 32;
 #pragma unroll 4
       for (int vi = ct; vi < nvec; vi += kThreads) {
-        const int row = p.vpt_shift >= 0 ? (vi >> p.vpt_shift) : (vi / p.vpt);
+        const int row = vec_row(p, vi);
         const int w = vi - row * p.vpt;
         char* d = reinterpret_cast<char*>(tab[row]);
         if (d) {

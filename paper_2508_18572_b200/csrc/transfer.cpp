@@ -154,6 +154,22 @@ void fill_table(const strata_xfer* x, const Plan& plan, const Batch& b, strata::
   }
 }
 
+// Division by the vectors-per-row count of a non-power-of-two row (MLA latents: 1152 B = 72
+// vectors) costs a ~20-instruction integer division per 16-byte vector in the LDG loops; a
+// multiply-high by ceil(2^32 / d) is exact for every n < n_max when it is exact at the largest n
+// of each quotient (its error grows with n), which is checked here.
+uint32_t div_magic(int d, int n_max) {
+  if (d <= 1 || n_max <= 0) return 0;
+  const uint64_t m = (uint64_t(1) << 32) / uint64_t(d) + 1;
+  if (m > 0xffffffffull) return 0;
+  for (int64_t q = 0; q * d < n_max; ++q) {
+    const int64_t n = std::min<int64_t>(n_max - 1, q * d + d - 1);
+    if (static_cast<int64_t>((uint64_t(n) * m) >> 32) != q || static_cast<int64_t>((uint64_t(q * d) * m) >> 32) != q)
+      return 0;
+  }
+  return static_cast<uint32_t>(m);
+}
+
 int ilog2_exact(int v) {
   if (v <= 0 || (v & (v - 1))) return -1;
   int s = 0;
@@ -213,7 +229,7 @@ static bool env_validate() {
 
 static void count_op(strata_pool* p, const Plan& plan, const strata_xfer* x, int engine) {
   p->counters.operations += 1;
-  p->counters.bytes += 2 * plan.total_tokens * p->tok_bytes * (x->layer_end - x->layer_begin);
+  p->counters.bytes += p->nkv * plan.total_tokens * p->tok_bytes * (x->layer_end - x->layer_begin);
   p->counters.last_engine = engine;
 }
 
@@ -240,6 +256,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.head_bytes = static_cast<int32_t>(p->head_bytes);
   xp.vpt = xp.tok_bytes / 16;
   xp.vpt_shift = ilog2_exact(xp.vpt);
+  xp.vpt_magic = xp.vpt_shift < 0 ? div_magic(xp.vpt, 32 * xp.vpt) : 0;
   xp.vph = xp.head_bytes / 16;
   xp.c_shift = ilog2_exact(xp.C);
   xp.p_shift = ilog2_exact(xp.P);
@@ -251,6 +268,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.host = p->host_dev;
   xp.host_chunks = x->host_chunks;
   xp.dev_pages = x->dev_pages;
+  xp.nkv = p->nkv;
 
   int engine = x->engine;
   if (engine == STRATA_ENGINE_DEFAULT) {
@@ -259,7 +277,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     // amortised and the zero-copy LDG kernel wins.  Without a host mirror of the chunk list only
     // the kernel engines can run.
     // (Offloads group layers into >= 128 KiB runs inside the DMA engine, see transfer_dma.)
-    const int64_t layer_bytes = 2 * plan.total_tokens * p->tok_bytes;
+    const int64_t layer_bytes = p->nkv * plan.total_tokens * p->tok_bytes;
     const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes;
     engine = dma ? STRATA_ENGINE_DMA : STRATA_ENGINE_LDG;
   }
@@ -327,7 +345,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   // per-layer launches.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   const int64_t fgroups = plan.batches.empty() ? 0
-                              : (2LL * plan.batches[0].ntok + xp.rows_per_group - 1) / xp.rows_per_group;
+                              : (int64_t(p->nkv) * plan.batches[0].ntok + xp.rows_per_group - 1) / xp.rows_per_group;
   const int fctas = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctas, (fgroups * 32 + threads - 1) / threads)));
   if (engine == STRATA_ENGINE_LDG && plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 &&
       (fctas >= 2 || fused_mode() == 2) && L <= kMaxFusedLayers && fused_mode() && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
@@ -371,11 +389,11 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
     xp.kbase = static_cast<char*>(p->k[l]);
     xp.vbase = static_cast<char*>(p->v[l]);
-    xp.layer_off = int64_t(l) * 2 * p->d.chunk_tokens * p->tok_bytes;
+    xp.layer_off = int64_t(l) * p->nkv * p->d.chunk_tokens * p->tok_bytes;
     for (const Batch& b : plan.batches) {
       xp.ntok = b.ntok;
       fill_table(x, plan, b, xp.rt);
-      const int64_t rows = 2LL * b.ntok;
+      const int64_t rows = int64_t(p->nkv) * b.ntok;
       int c = ctas;
       if (engine != STRATA_ENGINE_LDG) {
         const int64_t pieces = (rows + xp.tma_rows - 1) / xp.tma_rows;

@@ -40,7 +40,9 @@ class GpuCase:
             self.v = [torch.randint(0, 256, (self.layer_bytes,), dtype=torch.uint8, device="cuda", generator=gen)
                       for _ in range(g.L)]
         self.pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P,
-                                chunk_tokens=g.C, k_ptrs=self.k, v_ptrs=self.v, num_pages=g.num_pages,
+                                chunk_tokens=g.C, k_ptrs=self.k,
+                                # KV = 1 (MLA latent): one buffer per layer; self.v stays canary
+                                v_ptrs=None if getattr(g, "kv", 2) == 1 else self.v, num_pages=g.num_pages,
                                 num_chunks=g.num_chunks, flags=flags,
                                 strides=(0, 0, 0) if strides is None else strides)
         if host_fill == "random":

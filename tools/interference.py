@@ -75,6 +75,9 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--groups", default="0", help="DMA layer_group values (engine 4 only)")
     ap.add_argument("--memcpy", type=int, default=0, help="also co-run a contiguous cudaMemcpyAsync loop (-1 engine)")
+    ap.add_argument("--graph", type=int, default=0,
+                    help="replay each proxy from a CUDA graph (as serving engines run decode): copy-engine "
+                         "traffic delays the per-kernel launch fetches of eager proxies (ce_interference.py)")
     args = ap.parse_args()
 
     g = kvgen.geometry("llama8b_32k")
@@ -90,6 +93,17 @@ def main():
     io = torch.cuda.Stream(priority=hi)       # I/O: high priority (its few CTAs get SMs first)
     comp = torch.cuda.Stream(priority=lo)
     proxies = {"prefill": make_prefill(), "decode": make_decode()}
+    if args.graph:
+        graphs = {}
+        for name, fn in proxies.items():
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(comp):
+                fn()
+                torch.cuda.synchronize()
+                with torch.cuda.graph(gr, stream=comp):
+                    fn()
+            graphs[name] = gr
+        proxies = {name: gr.replay for name, gr in graphs.items()}
     alone = {name: time_proxy(fn, comp, args.reps) for name, fn in proxies.items()}
     print(json.dumps({"kind": "proxy_alone", **{k_: round(v_, 4) for k_, v_ in alone.items()}}), flush=True)
 
@@ -134,7 +148,7 @@ def main():
                 t_co = time_proxy(fn, comp, args.reps)
                 b.synchronize()
                 io_co = n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
-                print(json.dumps({"kind": "corun", "engine": eng, "ctas": c, "layer_group": G, "proxy": name,
+                print(json.dumps({"kind": "corun", "graph": args.graph, "engine": eng, "ctas": c, "layer_group": G, "proxy": name,
                                   "proxy_alone_ms": round(alone[name], 4), "proxy_corun_ms": round(t_co, 4),
                                   "slowdown": round(t_co / alone[name] - 1, 4), "io_alone_gbs": round(io_alone, 2),
                                   "io_corun_gbs_upper": round(io_co, 2)}), flush=True)
