@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--page-size", type=int, default=None)
     ap.add_argument("--engine", type=int, default=0, help="0 default, 1 LDG, 2 TMA")
     ap.add_argument("--num-ctas", type=int, default=0)
+    ap.add_argument("--layer-group", type=int, default=0, help="DMA engine: layers per copy run (0 = library default)")
     ap.add_argument("--frag", default="perm", choices=["perm", "churn"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
@@ -240,7 +241,8 @@ def main():
     io = torch.cuda.Stream()
 
     def step():
-        return pool.load(reqs, 0, g.L, stream=io, engine=args.engine, num_ctas=args.num_ctas)
+        return pool.load(reqs, 0, g.L, stream=io, engine=args.engine, num_ctas=args.num_ctas,
+                         layer_group=args.layer_group)
 
     def barrier():
         if world > 1:
@@ -388,6 +390,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "engine": engine_used, "num_ctas": args.num_ctas or "default",
+            "layer_group": args.layer_group or "default",
             "other_engines_gbs": others,
             "shared_gpu_test_mode": share or None,
             "zero_copy_kernels": zc,

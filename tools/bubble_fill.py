@@ -47,6 +47,8 @@ def main():
     ap.add_argument("--new", default="256,1024,4096")
     ap.add_argument("--engines", default="4,1")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--graph", type=int, default=0,
+                    help="replay each decode step from a CUDA graph, as serving engines run decode")
     args = ap.parse_args()
 
     g = kvgen.geometry("llama8b_32k")
@@ -68,6 +70,16 @@ def main():
             dec_kv[l].sum(dtype=torch.float32)
             for w in weights:
                 torch.matmul(dec_act[w.shape[0]], w)
+
+    if args.graph:
+        eager_step = decode_step
+        dg = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(comp):
+            eager_step()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(dg, stream=comp):
+                eager_step()
+        decode_step = dg.replay  # noqa: F811
 
     def timed(fn, stream):
         a, b = ev(), ev()
@@ -126,7 +138,7 @@ def main():
                 res[policy] = (statistics.median(spans), statistics.median(loads))
             pf, bf = res["prefill_first"], res["bubble_fill"]
             print(json.dumps({
-                "new": new, "cached": q.total_tokens, "load_compute_ratio": round(q.total_tokens / new, 1),
+                "new": new, "cached": q.total_tokens, "decode_graph": args.graph, "load_compute_ratio": round(q.total_tokens / new, 1),
                 "engine": {1: "ldg", 4: "dma"}.get(eng, eng), "load_alone_ms": round(t_load, 3),
                 "prefill_alone_ms": round(t_comp, 3), "decode_step_alone_ms": round(t_step, 3),
                 "bubble_steps": steps, "prefill_first_ms": round(pf[0], 3), "bubble_fill_ms": round(bf[0], 3),
