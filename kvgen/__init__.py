@@ -44,6 +44,16 @@ class Geometry:
     num_pages: int
     num_chunks: int
     kv: int = 2   # KV buffers per layer: 2 (K and V: MHA/GQA), 1 (MLA's shared latent, R27)
+    # Host tier heads (R28): the tier holds Ht >= H heads per token (0 = H) and this GPU
+    # moves heads [h0, h0+H) of them; head_major stores each chunk-layer as [KV][Ht][C][D] instead
+    # of the token-major [KV][C][Ht][D], so one head slice of a chunk-layer is one contiguous run.
+    Ht: int = 0
+    h0: int = 0
+    head_major: bool = False
+
+    @property
+    def host_heads(self) -> int:
+        return self.Ht or self.H
 
     @property
     def token_bytes(self) -> int:
@@ -52,8 +62,9 @@ class Geometry:
 
     @property
     def chunk_bytes(self) -> int:
-        """One host chunk holds C tokens of every layer's K and V: L*kv*C*S_tok bytes."""
-        return self.L * self.kv * self.C * self.token_bytes
+        """One host chunk holds C tokens of every layer's K and V for all Ht host heads:
+        L*kv*C*Ht*D*e bytes."""
+        return self.L * self.kv * self.C * self.host_heads * self.D * self.e
 
     @property
     def host_bytes(self) -> int:

@@ -40,7 +40,7 @@ def build(force: bool = False) -> str:
 class _Geom(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("L", "H", "D", "e", "P", "C", "page_stride", "token_stride", "head_stride",
-                 "num_pages", "num_chunks", "KV")]
+                 "num_pages", "num_chunks", "KV", "Ht", "h0", "head_major")]
 
 
 class _Reqs(ctypes.Structure):
@@ -75,7 +75,8 @@ def _ptr(a: np.ndarray) -> int:
 def _prep(g, host, k_imgs, v_imgs, q, l0, l1, strides):
     tok = g.H * g.D * g.e
     ps, ts, hs = strides or (g.P * tok, tok, g.D * g.e)
-    geom = _Geom(g.L, g.H, g.D, g.e, g.P, g.C, ps, ts, hs, g.num_pages, g.num_chunks, getattr(g, "kv", 2))
+    geom = _Geom(g.L, g.H, g.D, g.e, g.P, g.C, ps, ts, hs, g.num_pages, g.num_chunks, getattr(g, "kv", 2),
+                 getattr(g, "Ht", 0) or g.H, getattr(g, "h0", 0), int(getattr(g, "head_major", False)))
     keep = [np.ascontiguousarray(q.num_tokens, np.int64), np.ascontiguousarray(q.host_chunks, np.int32),
             np.ascontiguousarray(q.chunk_start, np.int64), np.ascontiguousarray(q.dev_pages, np.int32),
             np.ascontiguousarray(q.page_start, np.int64), np.ascontiguousarray(q.chunk_offset, np.int32),

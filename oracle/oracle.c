@@ -14,8 +14,14 @@
  *
  *   ci = off_c[r] + i;  hc = host_chunks[chunk_start[r] + ci / C];  ho = ci % C
  *   pi = off_p[r] + i;  pg = dev_pages [page_start [r] + pi / P];  po = pi % P
- *   src(l,kv,h) = host + hc*chunk_bytes + ((l*KV + kv)*C + ho)*H*D*e + h*D*e,  chunk_bytes = L*KV*C*H*D*e
+ *   src(l,kv,h) = host + hc*chunk_bytes + ((l*KV + kv)*C + ho)*Ht*D*e + (h0 + h)*D*e   (token-major)
+ *   src(l,kv,h) = host + hc*chunk_bytes + (((l*KV + kv)*Ht + h0 + h)*C + ho)*D*e   (head-major)
+ *   chunk_bytes = L*KV*C*Ht*D*e
  *   dst(l,kv,h) = pool[l][kv] + pg*page_stride + po*token_stride + h*head_stride
+ *
+ *   The host tier holds Ht >= H heads per token; this GPU moves heads [h0, h0+H) (R28:
+ *   Ht = H, h0 = 0 is the per-GPU tier of R13; a shared tier read by every TP rank has Ht = all
+ *   KV heads).  Token-major is R1's [L][KV][C][Ht][D] chunk; head-major keeps [L][KV][Ht][C][D].
  *
  *   KV = 2 (a K and a V buffer per layer, MHA/GQA) or KV = 1 (one buffer per layer: MLA's latent
  *   cache, where K and V are both derived from one compressed vector per token — DESIGN.md R27).
@@ -51,6 +57,8 @@ typedef struct {
     int64_t num_pages;         /* device capacity in pages */
     int64_t num_chunks;        /* host capacity in chunks */
     int64_t KV;                /* buffers per layer: 2 (K, V) or 1 (MLA latent) */
+    int64_t Ht, h0;            /* host heads per token (>= H) and this GPU's first head */
+    int64_t head_major;        /* 0: chunk-layer = [C][Ht][D]; 1: [Ht][C][D] */
 } oracle_geom;
 
 typedef struct {
@@ -69,8 +77,7 @@ typedef struct {
 static int oracle_move(const oracle_geom* g, uint8_t* host, uint8_t* const* k_img,
                        uint8_t* const* v_img, const oracle_reqs* q, int dir, int nthreads) {
     const int64_t row_bytes = g->D * g->e;            /* one head of one token */
-    const int64_t tok_bytes = g->H * g->D * g->e;      /* S_tok */
-    const int64_t chunk_bytes = g->L * g->KV * g->C * tok_bytes;
+    const int64_t chunk_bytes = g->L * g->KV * g->C * g->Ht * row_bytes;
     int bad = 0;
     (void)nthreads;
     for (int64_t r = 0; r < q->R; ++r) {
@@ -95,8 +102,10 @@ static int oracle_move(const oracle_geom* g, uint8_t* host, uint8_t* const* k_im
                 for (int64_t kv = 0; kv < g->KV; ++kv) {
                     uint8_t* pool = kv == 0 ? k_img[l] : v_img[l];
                     for (int64_t h = 0; h < g->H; ++h) {
-                        uint8_t* hp = host + hc * chunk_bytes + ((l * g->KV + kv) * g->C + ho) * tok_bytes +
-                                      h * row_bytes;
+                        const int64_t lkv = l * g->KV + kv;
+                        uint8_t* hp = host + hc * chunk_bytes +
+                                      (g->head_major ? ((lkv * g->Ht + g->h0 + h) * g->C + ho) * row_bytes
+                                                     : (lkv * g->C + ho) * g->Ht * row_bytes + (g->h0 + h) * row_bytes);
                         uint8_t* dp = pool + pg * g->page_stride + po * g->token_stride +
                                       h * g->head_stride;
                         if (dir == 0) memcpy(dp, hp, (size_t)row_bytes);
