@@ -16,6 +16,7 @@ infrastructure) on the host cores instead.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -71,6 +72,8 @@ def workload(args, rank: int, world: int):
     """Per-rank geometry + request tables (replicas of the config; the TP config is already the
     per-rank head slice)."""
     g = kvgen.geometry(args.config, P=args.page_size)
+    if g.host_heads > g.H:   # a shared tier holding every KV head: this rank moves head slice `rank`
+        g = dataclasses.replace(g, h0=(rank % (g.host_heads // g.H)) * g.H)
     n = kvgen.CONFIGS[args.config]["n"]
     rng = kvgen.rng_for(args.seed * 1000 + rank)
     if args.frag == "perm":
@@ -196,7 +199,8 @@ def run_reference(args):
 
 def _config(args, g, q):
     return {"workload": args.config, "layers": g.L, "kv_heads_per_gpu": g.H, "head_dim": g.D, "kv_dtype": "bf16",
-            "kv_buffers_per_layer": g.kv,
+            "kv_buffers_per_layer": g.kv, "host_heads": g.host_heads, "head_begin": g.h0,
+            "host_layout": "head-major" if g.head_major else "token-major",
             "page_size": g.P, "host_chunk_tokens": g.C, "tokens_per_gpu": q.total_tokens,
             "requests": q.R, "fragmentation": args.frag, "bytes_per_step_per_gpu": g.kv * g.L * q.total_tokens * g.token_bytes,
             "l2": f"no flush: each step moves {g.kv * g.L * q.total_tokens * g.token_bytes / 2**30:.1f} GiB, "
@@ -234,7 +238,8 @@ def main():
     v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)] if g.kv == 2 else k
     pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
                        k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=g.num_pages,
-                       num_chunks=g.num_chunks, device=local)
+                       num_chunks=g.num_chunks, device=local, host_heads=g.Ht, head_begin=g.h0,
+                       head_major=g.head_major)
     kvgen.fill_random(pool.host, args.seed * 1000 + rank)
     reqs = st.Requests.from_kvgen(q, device=local)
     bytes_step = g.kv * g.L * q.total_tokens * g.token_bytes

@@ -15,10 +15,16 @@
  *
  * LAYOUTS (DESIGN.md §3 readings R1-R5)
  *   Host tier, page-first ("arranges layers of a page contiguously"):
- *     num_chunks chunks of C tokens; chunk = [L][K,V][C][H][D] elements of e bytes,
- *     chunk_bytes = L*KV*C*H*D*e.  Token ho of chunk hc, layer l, kv, head h starts at
- *       host_base + hc*chunk_bytes + ((l*KV + kv)*C + ho)*H*D*e + h*D*e.
+ *     num_chunks chunks of C tokens; chunk = [L][K,V][C][Ht][D] elements of e bytes,
+ *     chunk_bytes = L*KV*C*Ht*D*e.  This GPU moves heads [h0, h0+H) of the tier's Ht heads
+ *     (host_heads, head_begin; default Ht = H, h0 = 0: a per-GPU tier).  Token ho of chunk hc,
+ *     layer l, kv, this GPU's head h starts at
+ *       host_base + hc*chunk_bytes + ((l*KV + kv)*C + ho)*Ht*D*e + (h0 + h)*D*e         (token-major)
+ *       host_base + hc*chunk_bytes + ((((h0 + h)*L + l)*KV + kv)*C + ho)*D*e           (head-major)
  *     KV = 2 (a K and a V buffer per layer), or KV = 1 with STRATA_POOL_SINGLE_KV (R27).
+ *     STRATA_HOST_HEAD_MAJOR stores each chunk as [Ht][L][K,V][C][D] (R28): every head's part is a
+ *     one-head page-first chunk, so a single tier holding every KV head serves any tensor-parallel
+ *     degree with the same long runs (K and V of C tokens per layer and head) as a per-GPU tier.
  *   Device pool, layer-first, paged: one K and one V buffer per layer,
  *     caller-owned; token slot (page pg, offset po < P), head h starts at
  *       {k,v}_ptrs[l] + pg*page_stride + po*token_stride + h*head_stride.
@@ -82,8 +88,9 @@ enum strata_pool_flags {
   STRATA_HOST_NO_NUMA_BIND = 8,  /* do not bind library-allocated host memory to the GPU's node */
   STRATA_HOST_CUDA_ALLOC = 16,   /* library-allocated host tier via cudaHostAlloc(Mapped|Portable)
                                     instead of mmap + cudaHostRegister */
-  STRATA_POOL_SINGLE_KV = 32     /* one KV buffer per layer (MLA latent cache, KV = 1 in LAYOUTS);
+  STRATA_POOL_SINGLE_KV = 32,    /* one KV buffer per layer (MLA latent cache, KV = 1 in LAYOUTS);
                                     v_ptrs is ignored */
+  STRATA_HOST_HEAD_MAJOR = 64    /* host chunks are [Ht][L][K,V][C][D] (LAYOUTS, R28) */
 };
 
 /* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
@@ -119,6 +126,9 @@ typedef struct {
   int64_t num_pages;              /* device capacity in pages (>= 1) */
   void* host_base;                /* caller host memory to register, or NULL: library allocates */
   int64_t num_chunks;             /* host capacity in chunks (>= 1) */
+  int32_t host_heads;             /* Ht: heads per token in the host tier (0 = num_heads) */
+  int32_t head_begin;             /* h0: first host head this GPU moves; h0 + num_heads <= Ht.
+                                     With Ht > num_heads or head-major chunks, D*e % 16 == 0. */
 } strata_pool_desc;
 
 typedef struct {

@@ -45,8 +45,8 @@ class Geometry:
     num_chunks: int
     kv: int = 2   # KV buffers per layer: 2 (K and V: MHA/GQA), 1 (MLA's shared latent, R27)
     # Host tier heads (R28): the tier holds Ht >= H heads per token (0 = H) and this GPU
-    # moves heads [h0, h0+H) of them; head_major stores each chunk-layer as [KV][Ht][C][D] instead
-    # of the token-major [KV][C][Ht][D], so one head slice of a chunk-layer is one contiguous run.
+    # moves heads [h0, h0+H) of them; head_major stores a chunk as [Ht][L][KV][C][D] instead of the
+    # token-major [L][KV][C][Ht][D]: each head's part is a one-head page-first chunk.
     Ht: int = 0
     h0: int = 0
     head_major: bool = False
@@ -92,6 +92,10 @@ CONFIGS: Dict[str, dict] = {
     # DeepSeek-V3 MLA latent cache (one buffer per layer: kv_lora_rank 512 + rope 64 = 576 bf16 per
     # token; 61 layers), 32K-token prefix.  A variant beyond BASELINE.json's configs;
     # the latent is replicated, not head-sharded, under TP, so multi-GPU runs are replicas.
+    # Llama-3.1-70B TP=8 from ONE host tier holding all 8 KV heads in head-major chunks (R28): each
+    # rank moves its head h0 = rank of it; 32K-token prefix (a 12.5 GiB shared tier).
+    "llama70b_tp8_shared": dict(L=80, H=1, D=128, e=2, P=1, C=64, n=[32768], num_pages=40960,
+                                num_chunks=640, tp=8, Ht=8, head_major=True),
     "deepseek_v3_mla": dict(L=61, H=1, D=576, e=2, P=1, C=64, n=[32768], num_pages=40960,
                             num_chunks=640, tp=1, kv=1),
 }
@@ -106,7 +110,8 @@ def geometry(name: str, P: Optional[int] = None, **over) -> Geometry:
         c["num_pages"] = -(-slots // P)
         c["P"] = P
     return Geometry(L=c["L"], H=c["H"], D=c["D"], e=c["e"], P=c["P"], C=c["C"],
-                    num_pages=c["num_pages"], num_chunks=c["num_chunks"], kv=c.get("kv", 2))
+                    num_pages=c["num_pages"], num_chunks=c["num_chunks"], kv=c.get("kv", 2), Ht=c.get("Ht", 0),
+                    h0=c.get("h0", 0), head_major=c.get("head_major", False))
 
 
 def rng_for(seed: int) -> np.random.Generator:

@@ -15,13 +15,14 @@
  *   ci = off_c[r] + i;  hc = host_chunks[chunk_start[r] + ci / C];  ho = ci % C
  *   pi = off_p[r] + i;  pg = dev_pages [page_start [r] + pi / P];  po = pi % P
  *   src(l,kv,h) = host + hc*chunk_bytes + ((l*KV + kv)*C + ho)*Ht*D*e + (h0 + h)*D*e   (token-major)
- *   src(l,kv,h) = host + hc*chunk_bytes + (((l*KV + kv)*Ht + h0 + h)*C + ho)*D*e   (head-major)
+ *   src(l,kv,h) = host + hc*chunk_bytes + (((h0 + h)*L + l)*KV + kv)*C*D*e + ho*D*e   (head-major)
  *   chunk_bytes = L*KV*C*Ht*D*e
  *   dst(l,kv,h) = pool[l][kv] + pg*page_stride + po*token_stride + h*head_stride
  *
  *   The host tier holds Ht >= H heads per token; this GPU moves heads [h0, h0+H) (R28:
  *   Ht = H, h0 = 0 is the per-GPU tier of R13; a shared tier read by every TP rank has Ht = all
- *   KV heads).  Token-major is R1's [L][KV][C][Ht][D] chunk; head-major keeps [L][KV][Ht][C][D].
+ *   KV heads).  Token-major is R1's [L][KV][C][Ht][D] chunk; head-major keeps [Ht][L][KV][C][D]:
+ *   every head's part of a chunk is itself a one-head page-first chunk.
  *
  *   KV = 2 (a K and a V buffer per layer, MHA/GQA) or KV = 1 (one buffer per layer: MLA's latent
  *   cache, where K and V are both derived from one compressed vector per token — DESIGN.md R27).
@@ -58,7 +59,7 @@ typedef struct {
     int64_t num_chunks;        /* host capacity in chunks */
     int64_t KV;                /* buffers per layer: 2 (K, V) or 1 (MLA latent) */
     int64_t Ht, h0;            /* host heads per token (>= H) and this GPU's first head */
-    int64_t head_major;        /* 0: chunk-layer = [C][Ht][D]; 1: [Ht][C][D] */
+    int64_t head_major;        /* 0: chunk = [L][KV][C][Ht][D]; 1: [Ht][L][KV][C][D] */
 } oracle_geom;
 
 typedef struct {
@@ -104,7 +105,7 @@ static int oracle_move(const oracle_geom* g, uint8_t* host, uint8_t* const* k_im
                     for (int64_t h = 0; h < g->H; ++h) {
                         const int64_t lkv = l * g->KV + kv;
                         uint8_t* hp = host + hc * chunk_bytes +
-                                      (g->head_major ? ((lkv * g->Ht + g->h0 + h) * g->C + ho) * row_bytes
+                                      (g->head_major ? (((g->h0 + h) * g->L * g->KV + lkv) * g->C + ho) * row_bytes
                                                      : (lkv * g->C + ho) * g->Ht * row_bytes + (g->h0 + h) * row_bytes);
                         uint8_t* dp = pool + pg * g->page_stride + po * g->token_stride +
                                       h * g->head_stride;

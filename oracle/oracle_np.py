@@ -23,13 +23,13 @@ def _host_view(host: np.ndarray, g) -> np.ndarray:
     """[num_chunks][L][KV][C][H][D*e] view of this GPU's heads [h0, h0+H) of the host tier.
 
     Token-major chunk: [L][K,V][C][Ht][D*e] ("arranges layers of a page contiguously", PAPER.md:286);
-    head-major chunk: [L][K,V][Ht][C][D*e], exposed token-major by swapping two axes (R28).
+    head-major chunk: [Ht][L][K,V][C][D*e], exposed token-major by moving the head axis (R28).
     """
     Ht = getattr(g, "Ht", 0) or g.H
     h0 = getattr(g, "h0", 0)
     if getattr(g, "head_major", False):
-        v = host.reshape(g.num_chunks, g.L, _kv(g), Ht, g.C, g.D * g.e)[:, :, :, h0:h0 + g.H]
-        return np.swapaxes(v, 3, 4)
+        v = host.reshape(g.num_chunks, Ht, g.L, _kv(g), g.C, g.D * g.e)[:, h0:h0 + g.H]
+        return np.moveaxis(v, 1, 4)
     return host.reshape(g.num_chunks, g.L, _kv(g), g.C, Ht, g.D * g.e)[:, :, :, :, h0:h0 + g.H]
 
 

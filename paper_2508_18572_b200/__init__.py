@@ -23,6 +23,7 @@ from . import _lib
 from ._lib import (STRATA_D2H, STRATA_ENGINE_DEFAULT, STRATA_ENGINE_LDG, STRATA_ENGINE_TMA,  # noqa: F401
                    STRATA_ENGINE_TMA_BULK, STRATA_ENGINE_DMA,
                    STRATA_H2D, STRATA_HOST_HUGEPAGES, STRATA_HOST_NO_NUMA_BIND, STRATA_POOL_SINGLE_KV,
+                   STRATA_HOST_HEAD_MAJOR,
                    STRATA_HOST_WRITECOMBINED, STRATA_VALIDATE, PoolDesc, StrataError, Xfer, check)
 
 __all__ = [
@@ -191,9 +192,11 @@ class HostPool:
     def __init__(self, *, num_layers: int, num_heads: int, head_dim: int, elem_bytes: int, page_size: int,
                  chunk_tokens: int, k_ptrs: Sequence, v_ptrs: Optional[Sequence], num_pages: int, num_chunks: int,
                  device: int = 0, flags: int = 0, host: Optional[np.ndarray] = None,
-                 strides=(0, 0, 0)):
+                 strides=(0, 0, 0), host_heads: int = 0, head_begin: int = 0, head_major: bool = False):
         def ptr(x):
             return int(x) if isinstance(x, int) else int(x.data_ptr())
+        if head_major:
+            flags |= STRATA_HOST_HEAD_MAJOR
         # v_ptrs=None: one buffer per layer (MLA latent cache, STRATA_POOL_SINGLE_KV)
         if v_ptrs is None:
             flags |= STRATA_POOL_SINGLE_KV
@@ -207,7 +210,7 @@ class HostPool:
                         v_ptrs=ctypes.cast(self._v, ctypes.POINTER(ctypes.c_void_p)),
                         page_stride=strides[0], token_stride=strides[1], head_stride=strides[2],
                         num_pages=num_pages, host_base=(host.ctypes.data if host is not None else None),
-                        num_chunks=num_chunks)
+                        num_chunks=num_chunks, host_heads=host_heads, head_begin=head_begin)
         self.handle = strata_register_host_pool(desc)
         self._hptr = ctypes.c_void_p(self.handle)
         self._ticket = ctypes.c_uint64()

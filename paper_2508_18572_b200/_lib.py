@@ -32,6 +32,7 @@ STRATA_VALIDATE = 4
 STRATA_HOST_NO_NUMA_BIND = 8
 STRATA_HOST_CUDA_ALLOC = 16
 STRATA_POOL_SINGLE_KV = 32
+STRATA_HOST_HEAD_MAJOR = 64
 
 STRATA_ENGINE_DEFAULT = 0
 STRATA_ENGINE_LDG = 1
@@ -65,6 +66,7 @@ class PoolDesc(ctypes.Structure):
         ("k_ptrs", ctypes.POINTER(ctypes.c_void_p)), ("v_ptrs", ctypes.POINTER(ctypes.c_void_p)),
         ("page_stride", ctypes.c_int64), ("token_stride", ctypes.c_int64), ("head_stride", ctypes.c_int64),
         ("num_pages", ctypes.c_int64), ("host_base", ctypes.c_void_p), ("num_chunks", ctypes.c_int64),
+        ("host_heads", ctypes.c_int32), ("head_begin", ctypes.c_int32),
     ]
 
 

@@ -111,6 +111,12 @@ int check_desc(const strata_pool_desc* d) {
                 (long long)ps, (long long)ts, (long long)hs);
   if (hs != head_bytes && head_bytes % 16)
     return fail(STRATA_ERR_ALIGNMENT, "non-contiguous heads need D*e %% 16 == 0");
+  const int64_t Ht = d->host_heads ? d->host_heads : d->num_heads;
+  if (d->host_heads < 0 || d->head_begin < 0 || d->head_begin + int64_t(d->num_heads) > Ht)
+    return fail(STRATA_ERR_INVALID_ARG, "head slice [%d,%d) not inside the host tier's %lld heads", d->head_begin,
+                d->head_begin + d->num_heads, (long long)Ht);
+  if ((Ht != d->num_heads || (d->flags & STRATA_HOST_HEAD_MAJOR)) && head_bytes % 16)
+    return fail(STRATA_ERR_ALIGNMENT, "a host head slice or head-major chunks need D*e %% 16 == 0");
   for (int l = 0; l < d->num_layers; ++l) {
     void* const vp = single ? d->k_ptrs[l] : d->v_ptrs[l];
     if (!d->k_ptrs[l] || !vp) return fail(STRATA_ERR_INVALID_ARG, "layer %d K/V pointer is NULL", l);
@@ -118,8 +124,9 @@ int check_desc(const strata_pool_desc* d) {
       return fail(STRATA_ERR_ALIGNMENT, "layer %d K/V pointer not 16-byte aligned", l);
   }
   if (d->host_base && !aligned16(d->host_base)) return fail(STRATA_ERR_ALIGNMENT, "host_base not 16-byte aligned");
-  const int64_t chunk = int64_t(d->num_layers) * nkv * d->chunk_tokens * tok;
-  if (chunk / tok / nkv / d->chunk_tokens != d->num_layers || d->num_chunks > INT64_MAX / chunk)
+  const int64_t htok = head_bytes * Ht;   // one token of one chunk-layer-kv block, all host heads
+  const int64_t chunk = int64_t(d->num_layers) * nkv * d->chunk_tokens * htok;
+  if (chunk / htok / nkv / d->chunk_tokens != d->num_layers || d->num_chunks > INT64_MAX / chunk)
     return fail(STRATA_ERR_INVALID_ARG, "host tier size overflows");
   return STRATA_OK;
 }
@@ -173,7 +180,21 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
   p->d.v_ptrs = p->v.data();
   p->head_bytes = int64_t(d->head_dim) * d->elem_bytes;
   p->tok_bytes = p->head_bytes * d->num_heads;
-  p->chunk_bytes = int64_t(d->num_layers) * p->nkv * d->chunk_tokens * p->tok_bytes;
+  p->host_heads = d->host_heads ? d->host_heads : d->num_heads;
+  p->head_begin = d->head_begin;
+  p->head_major = d->flags & STRATA_HOST_HEAD_MAJOR;
+  p->chunk_bytes = int64_t(d->num_layers) * p->nkv * d->chunk_tokens * p->host_heads * p->head_bytes;
+  if (p->head_major) {   // chunk = [Ht][L][KV][C][D]
+    p->host_kv_off = int64_t(d->chunk_tokens) * p->head_bytes;
+    p->host_tok_stride = p->head_bytes;
+    p->host_head_stride = int64_t(d->num_layers) * p->nkv * p->host_kv_off;
+    p->host_head_off = int64_t(p->head_begin) * p->host_head_stride;
+  } else {               // chunk = [L][KV][C][Ht][D]
+    p->host_kv_off = int64_t(d->chunk_tokens) * p->host_heads * p->head_bytes;
+    p->host_tok_stride = int64_t(p->host_heads) * p->head_bytes;
+    p->host_head_off = int64_t(p->head_begin) * p->head_bytes;
+    p->host_head_stride = p->head_bytes;
+  }
   p->token_stride = d->token_stride ? d->token_stride : p->tok_bytes;
   p->head_stride = d->head_stride ? d->head_stride : p->head_bytes;
   p->page_stride = d->page_stride ? d->page_stride : d->page_size * p->token_stride;

@@ -45,8 +45,13 @@ int for_each_copy(strata_pool_t p, const strata_xfer* x, int dir, F&& emit) {
   if (x->num_reqs > 0 && (!x->num_tokens || !x->chunk_start || !x->page_start))
     return bfail(STRATA_ERR_INVALID_ARG, "NULL request table");
   const int64_t C = p->d.chunk_tokens, P = p->d.page_size, tok = p->tok_bytes;
-  const bool rows_contig = p->head_stride == p->head_bytes;
-  const bool pages_contig = rows_contig && p->token_stride == tok;
+  // one copy per token row when the row's heads are adjacent on both sides; runs of tokens when
+  // consecutive tokens are adjacent on both sides too
+  const bool one_head = p->d.num_heads == 1;
+  const bool rows_contig = (p->head_stride == p->head_bytes || one_head) &&
+                           (p->host_head_stride == p->head_bytes || one_head);
+  const bool pages_contig = rows_contig && p->token_stride == tok && p->host_tok_stride == tok;
+  const int64_t kv_blk = p->host_kv_off;   // K -> V (and, times KV, layer) step in a chunk (R28)
   for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
     for (int kv = 0; kv < p->nkv; ++kv) {
       char* base = static_cast<char*>(kv ? p->v[l] : p->k[l]);
@@ -63,14 +68,15 @@ int for_each_copy(strata_pool_t p, const strata_xfer* x, int dir, F&& emit) {
             return bfail(STRATA_ERR_INDEX_RANGE, "index out of range");
           int64_t run = 1;
           if (pages_contig) run = std::min({n - i, C - ci % C, P - pi % P});
-          char* h = p->host + hc * p->chunk_bytes + ((int64_t(l) * p->nkv + kv) * C + ci % C) * tok;
+          char* h = p->host + hc * p->chunk_bytes + (int64_t(l) * p->nkv + kv) * kv_blk +
+                    (ci % C) * p->host_tok_stride + p->host_head_off;
           char* d = base + pg * p->page_stride + (pi % P) * p->token_stride;
           if (rows_contig) {
             if (dir == 0) emit(Copy{d, h, size_t(run * tok)});
             else emit(Copy{h, d, size_t(run * tok)});
           } else {
             for (int hh = 0; hh < p->d.num_heads; ++hh) {
-              char* hp = h + hh * p->head_bytes;
+              char* hp = h + hh * p->host_head_stride;
               char* dp = d + hh * p->head_stride;
               if (dir == 0) emit(Copy{dp, hp, size_t(p->head_bytes)});
               else emit(Copy{hp, dp, size_t(p->head_bytes)});

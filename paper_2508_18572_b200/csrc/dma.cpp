@@ -205,6 +205,14 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   xp.chunk_bytes = static_cast<int64_t>(gunit);
   xp.kv_off = C * tok;
   xp.host_chunks = p->slot_ids;
+  // staging keeps the host tier's order for this GPU's heads only: token-major [G][KV][C][H][D], or
+  // head-major [H][G][KV][C][D] (R28)
+  const bool hm = p->head_major;
+  const int64_t hb = p->head_bytes, Hl = p->d.num_heads, h0 = p->head_begin;
+  if (hm) xp.kv_off = C * hb;
+  xp.host_tok_stride = hm ? hb : tok;
+  xp.host_head_off = 0;
+  xp.host_head_stride = hm ? int64_t(G) * nkv * C * hb : hb;
 
   if ((e = cudaEventRecord(p->ev_fork, s))) return cuda_fail(e, "cudaEventRecord");
   for (int ci = 0; ci < p->ncs; ++ci)
@@ -235,7 +243,29 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
           src.push_back(dir == 0 ? h + off : d + off);
           sz.push_back(static_cast<size_t>(bytes));
         };
-        if (cp.lo == 0 && cp.cnt == C) {
+        if (hm) {
+          // head-major: head h0+hh of the chunk is a one-head page-first chunk [L][KV][C][D]
+          const int64_t lay = nkv * C * hb;   // one layer of one head
+          auto hoff = [&](int64_t hh, int g, int kv) {
+            return (h0 + hh) * p->host_head_stride + int64_t(lg + g) * lay + kv * C * hb;
+          };
+          auto soff = [&](int64_t hh, int g, int kv) { return (hh * G + g) * lay + kv * C * hb; };
+          char* const hbase = p->host + hc * p->chunk_bytes;
+          auto addh = [&](int64_t hofs, int64_t sofs, int64_t bytes) {
+            dst.push_back(dir == 0 ? d + sofs : hbase + hofs);
+            src.push_back(dir == 0 ? hbase + hofs : d + sofs);
+            sz.push_back(static_cast<size_t>(bytes));
+          };
+          for (int64_t hh = 0; hh < Hl; ++hh) {
+            if (cp.lo == 0 && cp.cnt == C) {
+              addh(hoff(hh, 0, 0), soff(hh, 0, 0), gl * lay);          // the group's layers: one run per head
+            } else {
+              for (int g = 0; g < gl; ++g)
+                for (int kv = 0; kv < nkv; ++kv)
+                  addh(hoff(hh, g, kv) + cp.lo * hb, soff(hh, g, kv) + cp.lo * hb, cp.cnt * hb);
+            }
+          }
+        } else if (cp.lo == 0 && cp.cnt == C) {
           add(0, gl * int64_t(unit));                  // the group's K,V runs are adjacent: one copy
         } else {
           for (int g = 0; g < gl; ++g) {
@@ -272,7 +302,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
         for (int g = 0; g < gl; ++g) {
           xp.kbase = static_cast<char*>(p->k[lg + g]);
           xp.vbase = static_cast<char*>(p->v[lg + g]);
-          xp.layer_off = int64_t(g) * int64_t(unit);
+          xp.layer_off = hm ? int64_t(g) * nkv * C * hb : int64_t(g) * int64_t(unit);
           cudaError_t le = strata::launch_ldg(xp, kdir, c, threads, unroll, s);
           if (le != cudaSuccess) return le;
           ++p->counters.kernel_launches;

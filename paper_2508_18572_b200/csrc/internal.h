@@ -39,6 +39,7 @@ struct XferParams {
   int32_t vpt_shift;            // log2(vpt) if vpt is a power of two, else -1
   uint32_t vpt_magic;           // else: row = umulhi(idx, vpt_magic) exactly for idx < 32*vpt (0 = divide)
   int32_t vph;                  // 16-byte vectors per head = head_bytes/16
+  int32_t vph_shift;            // log2(vph) if a power of two, else -1
   int32_t rows_per_group;       // LDG engine: token rows handled by one warp iteration (<= 32)
   int32_t tma_rows;             // TMA engine: token rows per pipeline stage (<= 32)
   int32_t tma_stages;           // TMA engine: pipeline depth
@@ -46,8 +47,12 @@ struct XferParams {
   int32_t c_shift, p_shift;     // log2(C), log2(P) when powers of two, else -1
   int64_t chunk_bytes;          // L*KV*C*S_tok
   int64_t layer_off;            // byte offset of (layer, K) inside a host chunk: l*KV*C*S_tok
-  int64_t kv_off;               // byte offset from K to V inside a chunk layer: C*S_tok
+  int64_t kv_off;               // K -> V offset in the host tier: C*Ht*D*e (token-major), C*D*e (head-major)
   int64_t page_stride, token_stride, head_stride;
+  // host side of a row (R28): token cr, head h of a chunk-layer-kv block starts at
+  //   block + cr*host_tok_stride + host_head_off + h*host_head_stride
+  // token-major: (Ht*D*e, h0*D*e, D*e); head-major: (D*e, h0*L*KV*C*D*e, L*KV*C*D*e)
+  int64_t host_tok_stride, host_head_off, host_head_stride;
   // data
   char* host;                   // device-visible address of the host tier (UVA)
   char* kbase;                  // this layer's K buffer
@@ -109,6 +114,11 @@ struct strata_pool {
   std::vector<void*> k, v;
   int64_t tok_bytes, head_bytes, chunk_bytes;
   int32_t nkv = 2;                    // KV buffers per layer (1: STRATA_POOL_SINGLE_KV)
+  int32_t host_heads = 0, head_begin = 0;   // Ht, h0 (R28)
+  bool head_major = false;
+  int64_t host_kv_off = 0, host_tok_stride = 0, host_head_off = 0, host_head_stride = 0;
+  // a host row (this GPU's heads of one token) is tok_bytes contiguous: what the TMA rings need
+  bool host_row_contig() const { return host_head_stride == head_bytes || d.num_heads == 1; }
   int64_t page_stride, token_stride, head_stride;
   // host tier
   char* host = nullptr;               // host address
@@ -196,6 +206,7 @@ constexpr int kTmaStageTarget = 32 << 10;
 int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan);                     // transfer.cpp
 void fill_table(const strata_xfer* x, const Plan& plan, const Batch& b, ReqTable& rt);        // transfer.cpp
 int ilog2_exact(int v);                                                                       // transfer.cpp
+bool dma_runs_ok(const strata_pool* p);                                                       // transfer.cpp
 uint32_t div_magic(int d, int n_max);   // m with umulhi(n, m) == n / d for n < n_max, or 0  transfer.cpp
 int transfer(strata_pool* p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir); // transfer.cpp
 int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, XferParams xp, cudaStream_t s,

@@ -87,9 +87,9 @@ __device__ __forceinline__ RowIdx row_none() {
 
 __device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x, char* kbase, char* vbase,
                                            int64_t layer_off, char*& hp, char*& dp) {
-  // host: chunk hc, layer l, kv, token cr            (page-first)
+  // host: chunk hc, layer l, kv, token cr, this GPU's first head   (page-first; R28)
   hp = p.host + static_cast<int64_t>(x.hc) * p.chunk_bytes + layer_off + x.kv * p.kv_off +
-       static_cast<int64_t>(x.cr) * p.tok_bytes;
+       static_cast<int64_t>(x.cr) * p.host_tok_stride + p.host_head_off;
   // device: page pg, offset pr of this layer's K/V  (layer-first paged pool)
   dp = (x.kv ? vbase : kbase) + static_cast<int64_t>(x.pg) * p.page_stride +
        static_cast<int64_t>(x.pr) * p.token_stride;
@@ -116,7 +116,16 @@ __device__ __forceinline__ void st_vec(void* ptr, const int4& v) {
 // (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
 // One layer of the LDG engine for this warp: groups warp, warp + nwarps, ...  `nx` holds the
 // already-fetched indices of the warp's first group (identical for every layer).
-template <int U, bool CONTIG, int DIR>
+// Address of 16-byte vector w of a row on one side: rows whose heads are adjacent are contiguous;
+// otherwise head h = w / vph sits at h * stride (device HND / padded heads, head-major host tiers).
+template <bool CONTIG>
+__device__ __forceinline__ uint64_t row_vec(uint64_t base, int w, const XferParams& p, int64_t stride) {
+  if (CONTIG) return base + static_cast<uint64_t>(w) * 16;
+  const int h = p.vph_shift >= 0 ? (w >> p.vph_shift) : (w / p.vph);
+  return base + h * stride + static_cast<uint64_t>(w - h * p.vph) * 16;
+}
+
+template <int U, bool CONTIG, bool HCONTIG, int DIR>
 __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char* vbase, int64_t layer_off,
                                           RowIdx nx, int64_t warp, int64_t nwarps, int lane) {
   const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
@@ -148,14 +157,9 @@ __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char
         const int w = idx - rl * p.vpt;
         const uint64_t s = __shfl_sync(kFull, my_src, rl & 31);
         if (idx < nvec) {
-          const char* a;
-          if (DIR == 0 || CONTIG) {
-            a = reinterpret_cast<const char*>(s) + w * 16;
-          } else {
-            const int h = w / p.vph;
-            a = reinterpret_cast<const char*>(s) + h * p.head_stride + (w - h * p.vph) * 16;
-          }
-          v[j] = ld_stream(a);
+          const uint64_t a = DIR == 0 ? row_vec<HCONTIG>(s, w, p, p.host_head_stride)
+                                      : row_vec<CONTIG>(s, w, p, p.head_stride);
+          v[j] = ld_stream(reinterpret_cast<const void*>(a));
         }
       }
 #pragma unroll
@@ -165,14 +169,9 @@ __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char
         const int w = idx - rl * p.vpt;
         const uint64_t d = __shfl_sync(kFull, my_dst, rl & 31);
         if (idx < nvec) {
-          char* a;
-          if (DIR == 1 || CONTIG) {
-            a = reinterpret_cast<char*>(d) + w * 16;
-          } else {
-            const int h = w / p.vph;
-            a = reinterpret_cast<char*>(d) + h * p.head_stride + (w - h * p.vph) * 16;
-          }
-          st_vec(a, v[j]);
+          const uint64_t a = DIR == 0 ? row_vec<CONTIG>(d, w, p, p.head_stride)
+                                      : row_vec<HCONTIG>(d, w, p, p.host_head_stride);
+          st_vec(reinterpret_cast<void*>(a), v[j]);
         }
       }
     }
@@ -188,12 +187,12 @@ __device__ __forceinline__ RowIdx ldg_first(const XferParams& p, int64_t warp, i
 
 // LDG engine, one layer per launch.  DIR 0: host -> device, DIR 1: device -> host.  CONTIG: device
 // rows head-contiguous (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
-template <int U, bool CONTIG, int DIR>
+template <int U, bool CONTIG, bool HCONTIG, int DIR>
 __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __grid_constant__ XferParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  ldg_layer<U, CONTIG, DIR>(p, p.kbase, p.vbase, p.layer_off, ldg_first(p, warp, lane), warp, nwarps, lane);
+  ldg_layer<U, CONTIG, HCONTIG, DIR>(p, p.kbase, p.vbase, p.layer_off, ldg_first(p, warp, lane), warp, nwarps, lane);
 }
 
 // LDG engine, every layer of the operation in ONE launch (the persistent variant):
@@ -215,16 +214,16 @@ __device__ __forceinline__ void st_release(uint32_t* a, uint32_t v) {
   else asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
 }
 
-template <int U, bool CONTIG, int DIR>
+template <int U, bool CONTIG, bool HCONTIG, int DIR>
 __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const __grid_constant__ FusedParams fp) {
   const XferParams& p = fp.x;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const RowIdx first = ldg_first(p, warp, lane);
-  const int64_t layer_step = static_cast<int64_t>(p.nkv) * p.C * p.tok_bytes;
+  const int64_t layer_step = static_cast<int64_t>(p.nkv) * p.kv_off;
   for (int l = fp.l0; l < fp.l1; ++l) {
-    ldg_layer<U, CONTIG, DIR>(p, fp.kb[l], fp.vb[l], int64_t(l) * layer_step, first, warp, nwarps, lane);
+    ldg_layer<U, CONTIG, HCONTIG, DIR>(p, fp.kb[l], fp.vb[l], int64_t(l) * layer_step, first, warp, nwarps, lane);
     __syncwarp();
     if (lane == 0) {
       layer_fence<DIR>();
@@ -535,15 +534,21 @@ __global__ void validate_kernel(const __grid_constant__ ValidateParams v) {
   }
 }
 
-template <int U, bool CONTIG, int DIR>
-cudaError_t ldg_launch(const XferParams& p, int ctas, int threads, cudaStream_t s) {
-  ldg_kernel<U, CONTIG, DIR><<<ctas, threads, 0, s>>>(p);
+template <int U, int DIR>
+cudaError_t ldg_launch(const XferParams& p, bool contig, bool hcontig, int ctas, int threads, cudaStream_t s) {
+  if (contig && hcontig) ldg_kernel<U, true, true, DIR><<<ctas, threads, 0, s>>>(p);
+  else if (contig) ldg_kernel<U, true, false, DIR><<<ctas, threads, 0, s>>>(p);
+  else if (hcontig) ldg_kernel<U, false, true, DIR><<<ctas, threads, 0, s>>>(p);
+  else ldg_kernel<U, false, false, DIR><<<ctas, threads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
-template <int U, bool CONTIG, int DIR>
-cudaError_t ldg_fused_launch(const FusedParams& p, int ctas, int threads, cudaStream_t s) {
-  ldg_fused_kernel<U, CONTIG, DIR><<<ctas, threads, 0, s>>>(p);
+template <int U, int DIR>
+cudaError_t ldg_fused_launch(const FusedParams& p, bool contig, bool hcontig, int ctas, int threads, cudaStream_t s) {
+  if (contig && hcontig) ldg_fused_kernel<U, true, true, DIR><<<ctas, threads, 0, s>>>(p);
+  else if (contig) ldg_fused_kernel<U, true, false, DIR><<<ctas, threads, 0, s>>>(p);
+  else if (hcontig) ldg_fused_kernel<U, false, true, DIR><<<ctas, threads, 0, s>>>(p);
+  else ldg_fused_kernel<U, false, false, DIR><<<ctas, threads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -556,38 +561,30 @@ cudaError_t tma_launch(const XferParams& p, int ctas, cudaStream_t s) {
 
 }  // namespace
 
+// device / host rows contiguous: heads adjacent (or a single head) on that side
+static bool dev_contig(const XferParams& p) { return p.head_stride == p.head_bytes || p.H == 1; }
+static bool host_contig(const XferParams& p) { return p.host_head_stride == p.head_bytes || p.H == 1; }
+
 cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s) {
-  const bool contig = p.head_stride == p.head_bytes;
+  const bool contig = dev_contig(p), hcontig = host_contig(p);
   if (threads > 512) unroll = 4;  // U=8 needs > 64 registers per thread
-#define STRATA_LDG(U)                                                               \
-  if (unroll == U) {                                                                \
-    if (dir == 0) return contig ? ldg_launch<U, true, 0>(p, ctas, threads, s)       \
-                                : ldg_launch<U, false, 0>(p, ctas, threads, s);     \
-    return contig ? ldg_launch<U, true, 1>(p, ctas, threads, s)                     \
-                  : ldg_launch<U, false, 1>(p, ctas, threads, s);                   \
-  }
-  STRATA_LDG(4)
-  STRATA_LDG(8)
-#undef STRATA_LDG
+  if (unroll == 4) return dir == 0 ? ldg_launch<4, 0>(p, contig, hcontig, ctas, threads, s)
+                                   : ldg_launch<4, 1>(p, contig, hcontig, ctas, threads, s);
+  if (unroll == 8) return dir == 0 ? ldg_launch<8, 0>(p, contig, hcontig, ctas, threads, s)
+                                   : ldg_launch<8, 1>(p, contig, hcontig, ctas, threads, s);
   return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_ldg_fused(const FusedParams& p, int dir, int ctas, int threads, cudaStream_t s) {
-  const bool contig = p.x.head_stride == p.x.head_bytes;
-  if (threads > 512) {
-    if (dir == 0) return contig ? ldg_fused_launch<4, true, 0>(p, ctas, threads, s)
-                                : ldg_fused_launch<4, false, 0>(p, ctas, threads, s);
-    return contig ? ldg_fused_launch<4, true, 1>(p, ctas, threads, s)
-                  : ldg_fused_launch<4, false, 1>(p, ctas, threads, s);
-  }
-  if (dir == 0) return contig ? ldg_fused_launch<8, true, 0>(p, ctas, threads, s)
-                              : ldg_fused_launch<8, false, 0>(p, ctas, threads, s);
-  return contig ? ldg_fused_launch<8, true, 1>(p, ctas, threads, s)
-                : ldg_fused_launch<8, false, 1>(p, ctas, threads, s);
+  const bool contig = dev_contig(p.x), hcontig = host_contig(p.x);
+  if (threads > 512) return dir == 0 ? ldg_fused_launch<4, 0>(p, contig, hcontig, ctas, threads, s)
+                                     : ldg_fused_launch<4, 1>(p, contig, hcontig, ctas, threads, s);
+  return dir == 0 ? ldg_fused_launch<8, 0>(p, contig, hcontig, ctas, threads, s)
+                  : ldg_fused_launch<8, 1>(p, contig, hcontig, ctas, threads, s);
 }
 
 cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s) {
-  const bool contig = p.head_stride == p.head_bytes;
+  const bool contig = dev_contig(p);
   if (dir == 0 && warp_specialized) {
     const int smem = tma_buf_offset(p.tma_stages) + p.tma_stages * p.tma_stage_bytes;
     if (contig) tma_ws_load_kernel<true><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);

@@ -170,6 +170,11 @@ uint32_t div_magic(int d, int n_max) {
   return static_cast<uint32_t>(m);
 }
 
+// Copy-engine runs need the GPU's host data of a chunk-layer in few long pieces: token-major
+// tiers holding only this GPU's heads (one run per chunk-layer), or head-major tiers (one run per
+// chunk-layer and head: K and V of C tokens, any head slice).
+bool dma_runs_ok(const strata_pool* p) { return p->head_major || p->host_heads == p->d.num_heads; }
+
 int ilog2_exact(int v) {
   if (v <= 0 || (v & (v - 1))) return -1;
   int s = 0;
@@ -258,10 +263,14 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.vpt_shift = ilog2_exact(xp.vpt);
   xp.vpt_magic = xp.vpt_shift < 0 ? div_magic(xp.vpt, 32 * xp.vpt) : 0;
   xp.vph = xp.head_bytes / 16;
+  xp.vph_shift = ilog2_exact(xp.vph);
   xp.c_shift = ilog2_exact(xp.C);
   xp.p_shift = ilog2_exact(xp.P);
   xp.chunk_bytes = p->chunk_bytes;
-  xp.kv_off = int64_t(p->d.chunk_tokens) * p->tok_bytes;
+  xp.kv_off = p->host_kv_off;
+  xp.host_tok_stride = p->host_tok_stride;
+  xp.host_head_off = p->host_head_off;
+  xp.host_head_stride = p->host_head_stride;
   xp.page_stride = p->page_stride;
   xp.token_stride = p->token_stride;
   xp.head_stride = p->head_stride;
@@ -278,9 +287,12 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     // the kernel engines can run.
     // (Offloads group layers into >= 128 KiB runs inside the DMA engine, see transfer_dma.)
     const int64_t layer_bytes = p->nkv * plan.total_tokens * p->tok_bytes;
-    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes;
+    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes && dma_runs_ok(p);
     engine = dma ? STRATA_ENGINE_DMA : STRATA_ENGINE_LDG;
   }
+  // the copy engines need long host runs: a token-major tier read in a head slice (Ht > H) has
+  // only H*D*e bytes per token contiguous, so its DMA requests run on the LDG engine instead
+  if (engine == STRATA_ENGINE_DMA && !dma_runs_ok(p)) engine = STRATA_ENGINE_LDG;
   if (engine == STRATA_ENGINE_DMA) {
     if (!x->host_chunks_host && plan.total_tokens > 0)
       return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
@@ -301,6 +313,9 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     if (ticket) *ticket = t;
     return STRATA_OK;
   }
+  // the TMA rings stage whole host rows: a head-major tier with > 1 head per GPU has none
+  if ((engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK) && !p->host_row_contig())
+    engine = STRATA_ENGINE_LDG;
   const bool tma = engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK;
   // TMA engine geometry: rows per stage (<= 32 lanes), stage bytes, depth
   if (tma) {
@@ -389,7 +404,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
     xp.kbase = static_cast<char*>(p->k[l]);
     xp.vbase = static_cast<char*>(p->v[l]);
-    xp.layer_off = int64_t(l) * p->nkv * p->d.chunk_tokens * p->tok_bytes;
+    xp.layer_off = int64_t(l) * p->nkv * xp.kv_off;
     for (const Batch& b : plan.batches) {
       xp.ntok = b.ntok;
       fill_table(x, plan, b, xp.rt);

@@ -46,6 +46,11 @@ static void cpu_checks(void) {
   d.token_stride = 264;
   EXPECT(strata_register_host_pool(&d, &p) == STRATA_ERR_ALIGNMENT, "token stride");
   d.token_stride = 0;
+  d.host_heads = 2; d.head_begin = 1;   /* heads [1,3) of a 2-head host tier (R28) */
+  EXPECT(strata_register_host_pool(&d, &p) == STRATA_ERR_INVALID_ARG, "head slice outside the host tier");
+  d.host_heads = 8; d.head_begin = 2; d.head_dim = 8; d.elem_bytes = 1; d.num_heads = 2;   /* D*e = 8 */
+  EXPECT(strata_register_host_pool(&d, &p) == STRATA_ERR_ALIGNMENT, "head slice needs D*e %% 16");
+  d.host_heads = 0; d.head_begin = 0; d.head_dim = 64; d.elem_bytes = 2;
   strata_xfer x;
   memset(&x, 0, sizeof x);
   EXPECT(strata_load(NULL, &x, NULL, NULL) == STRATA_ERR_INVALID_ARG, "NULL pool");

@@ -44,7 +44,9 @@ class GpuCase:
                                 # KV = 1 (MLA latent): one buffer per layer; self.v stays canary
                                 v_ptrs=None if getattr(g, "kv", 2) == 1 else self.v, num_pages=g.num_pages,
                                 num_chunks=g.num_chunks, flags=flags,
-                                strides=(0, 0, 0) if strides is None else strides)
+                                strides=(0, 0, 0) if strides is None else strides,
+                                host_heads=getattr(g, "Ht", 0), head_begin=getattr(g, "h0", 0),
+                                head_major=getattr(g, "head_major", False))
         if host_fill == "random":
             if g.host_bytes <= (64 << 20):
                 self.pool.host[:] = kvgen.random_bytes(rng, g.host_bytes)

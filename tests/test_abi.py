@@ -27,7 +27,7 @@ def test_exports_every_declared_symbol(lib):
 
 def test_struct_layouts_match_header(lib):
     # int32 x8 then pointers/int64 (see include/strata.h); 8-byte aligned, no padding surprises
-    assert ctypes.sizeof(PoolDesc) == 8 * 4 + 2 * 8 + 4 * 8 + 8 + 8
+    assert ctypes.sizeof(PoolDesc) == 8 * 4 + 2 * 8 + 4 * 8 + 8 + 8 + 2 * 4   # + host_heads, head_begin
     assert ctypes.sizeof(Xfer) == 6 * 4 + 7 * 8 + 2 * 8 + 8 + 8
 
 

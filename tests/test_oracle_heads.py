@@ -4,7 +4,7 @@
 A host tier may hold Ht >= H KV heads per token (e.g. every KV head of the model, shared by all
 tensor-parallel ranks, or written by a deployment with another TP degree); a GPU moves its heads
 [h0, h0+H).  Token-major chunks keep R1's [L][KV][C][Ht][D]; head-major chunks keep
-[L][KV][Ht][C][D], so one rank's slice of a chunk-layer is one contiguous run.  Pinned by:
+[Ht][L][KV][C][D], so each head's part of a chunk is a one-head page-first chunk.  Pinned by:
   * layout equivalence — a head-major tier built by numpy.transpose of a token-major tier loads to
     the same device bytes (ties head-major to the pinned token-major definition),
   * slicing        — a slice load equals the load from the compact per-rank tier cut out by numpy
@@ -32,7 +32,7 @@ def _geom(H=2, Ht=4, h0=1, head_major=False, L=2, D=16, e=2, P=2, C=4, kv=2, num
 
 def _to_head_major(host, g):
     v = host.reshape(g.num_chunks, g.L, g.kv, g.C, g.host_heads, g.D * g.e)
-    return np.ascontiguousarray(v.transpose(0, 1, 2, 4, 3, 5)).reshape(-1)
+    return np.ascontiguousarray(v.transpose(0, 4, 1, 2, 3, 5)).reshape(-1)
 
 
 def _load(oracle_mod, impl, g, host, q, l0=0, l1=None):
@@ -64,11 +64,12 @@ def test_slice_equals_compact_rank_tier(oracle_mod, impl, head_major):
     host = kvgen.random_bytes(rng, g.host_bytes)
     q = kvgen.make_requests(rng, [9, 17], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
     # the compact per-rank tier (Ht = H, h0 = 0, token-major) cut out with numpy slicing
-    shape = (g.num_chunks, g.L, g.kv) + ((g.host_heads, g.C) if head_major else (g.C, g.host_heads)) + (g.D * g.e,)
-    v = host.reshape(shape)
-    part = v[:, :, :, g.h0:g.h0 + g.H] if head_major else v[:, :, :, :, g.h0:g.h0 + g.H]
     if head_major:
-        part = part.transpose(0, 1, 2, 4, 3, 5)
+        v = host.reshape(g.num_chunks, g.host_heads, g.L, g.kv, g.C, g.D * g.e)
+        part = v[:, g.h0:g.h0 + g.H].transpose(0, 2, 3, 4, 1, 5)
+    else:
+        v = host.reshape(g.num_chunks, g.L, g.kv, g.C, g.host_heads, g.D * g.e)
+        part = v[:, :, :, :, g.h0:g.h0 + g.H]
     compact = np.ascontiguousarray(part).reshape(-1)
     g_rank = dataclasses.replace(g, Ht=0, h0=0, head_major=False)
     a = _load(oracle_mod, impl, g, host, q)
@@ -100,11 +101,12 @@ def test_tp_union_from_one_shared_tier(oracle_mod, head_major, T):
 def _tagged(g):
     vph = g.D * g.e // 16
     Ht = g.host_heads
-    order = (g.num_chunks, g.L, g.kv) + ((Ht, g.C) if g.head_major else (g.C, Ht)) + (vph,)
-    grids = np.meshgrid(*[np.arange(s, dtype=np.uint32) for s in order], indexing="ij")
-    c, l, kv = grids[:3]
-    h, t = (grids[3], grids[4]) if g.head_major else (grids[4], grids[3])
-    vec = grids[5]
+    if g.head_major:
+        order = (g.num_chunks, Ht, g.L, g.kv, g.C, vph)
+        c, h, l, kv, t, vec = np.meshgrid(*[np.arange(s, dtype=np.uint32) for s in order], indexing="ij")
+    else:
+        order = (g.num_chunks, g.L, g.kv, g.C, Ht, vph)
+        c, l, kv, t, h, vec = np.meshgrid(*[np.arange(s, dtype=np.uint32) for s in order], indexing="ij")
     tags = np.stack([c, (l << 1) | kv, t, (h << 16) | vec], axis=-1)
     return np.ascontiguousarray(tags).view(np.uint8).reshape(-1)
 
