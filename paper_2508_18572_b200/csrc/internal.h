@@ -202,11 +202,6 @@ constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;
 constexpr int kDefaultUnroll = 8;
 constexpr int kDefaultCtasTma = 2;   // warp-specialised ring: 51.0 GB/s at 2 CTAs (sweep_tma_ws15.jsonl)
 constexpr int kTmaStageTarget = 32 << 10;
-// warp-specialised TMA offload: small pieces (8 KiB) so each of its 15 gathering warps owns one
-// piece, and more stages than gathering warps + in-flight stores (kernels.cu kWsConsumers = 15,
-// kOffStores = 4)
-constexpr int kTmaOffStageTarget = 8 << 10;
-constexpr int kTmaOffMinStages = 15 + 4 + 1;
 
 int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan);                     // transfer.cpp
 void fill_table(const strata_xfer* x, const Plan& plan, const Batch& b, ReqTable& rt);        // transfer.cpp

@@ -273,8 +273,7 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 
 constexpr int kTmaHeader = 16 * kTmaMaxStages;           // mbarriers: full[32], empty[32]
 
-// per stage and lane: device row address, host row address (8 B each), host run length (4 B)
-__host__ __device__ constexpr int tma_table_bytes(int stages) { return stages * 32 * 20; }
+__host__ __device__ constexpr int tma_table_bytes(int stages) { return stages * 32 * 12; }
 __host__ __device__ constexpr int tma_buf_offset(int stages) {
   return (kTmaHeader + tma_table_bytes(stages) + 127) / 128 * 128;
 }
@@ -503,130 +502,6 @@ __global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel
 }
 
 // ---------------------------------------------------------------------------------------------
-// Warp-specialised TMA offload ("backup", PAPER.md:230, :262 — one CTA in the paper's design).
-// Warp 0 fetches each piece's indices and publishes its rows' device addresses and, per contiguous
-// host run, the host address and length (run detection as in tma_kernel).  Each of the
-// kWsConsumers LSU warps gathers WHOLE pieces (pieces round-robin over the warps, so 15 pieces'
-// HBM reads are in flight per CTA: a shared piece per CTA was HBM-latency bound at ~10 GB/s) into
-// the piece's shared-memory stage; warp 0 then writes every host run of the piece with ONE
-// cp.async.bulk store, in piece order, with up to kOffStores pieces' stores reading shared memory.
-// Requires S > kWsConsumers + kOffStores stages (transfer.cpp) so a warp never waits on a barrier
-// two phases ahead.
-constexpr int kOffStores = 4;
-
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void st_shared_v4(void* p, const int4& v) {
-  asm volatile("st.shared.v4.s32 [%0], {%1,%2,%3,%4};" :: "r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_read_off() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(kOffStores - 1) : "memory");
-}
-
-template <bool CONTIG>
-__global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_offload_kernel(const __grid_constant__ XferParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int S = p.tma_stages;
-  const int T = p.tma_rows;
-  const int SB = p.tma_stage_bytes;
-  const int tok = p.tok_bytes;
-  uint64_t* tab_full = reinterpret_cast<uint64_t*>(smem);       // warp 0 -> gatherer: tables ready
-  uint64_t* data_full = tab_full + kTmaMaxStages;                // gatherer -> warp 0: rows staged
-  uint64_t* tab_dev = reinterpret_cast<uint64_t*>(smem + kTmaHeader);   // [S][32]
-  uint64_t* tab_host = tab_dev + S * 32;                                   // [S][32]
-  int32_t* tab_len = reinterpret_cast<int32_t*>(tab_host + S * 32);        // [S][32]
-  unsigned char* buf = smem + tma_buf_offset(S);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&tab_full[s], 1);
-      mbar_init(&data_full[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
-  const int64_t npieces = (nrows + T - 1) / T;
-  const int64_t my = npieces > blockIdx.x ? (npieces - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t ahead = S - kOffStores;   // pieces published ahead of the store stream
-
-  if (warp == 0) {
-    auto fetch = [&](int64_t k) {
-      const int64_t row = (blockIdx.x + k * gridDim.x) * T + lane;
-      return (k < my && lane < T && row < nrows) ? row_fetch(p, row) : row_none();
-    };
-    RowIdx nx = fetch(0);
-    for (int64_t k = 0; k < my + ahead; ++k) {
-      if (k < my) {
-        const int s = static_cast<int>(k % S);
-        const RowIdx cur = nx;
-        nx = fetch(k + 1);
-        // stage s last held piece k-S; stores issued so far end at piece k-1-ahead, so waiting
-        // until <= kOffStores-1 groups still read shared memory frees it
-        if (k >= S) bulk_wait_read_off();
-        const bool valid = cur.kv >= 0;
-        char* hp = nullptr;
-        char* dp = nullptr;
-        if (valid) row_finish(p, cur, hp, dp);
-        const uint64_t hprev = __shfl_up_sync(kFull, reinterpret_cast<uint64_t>(hp), 1);
-        const int vprev = __shfl_up_sync(kFull, static_cast<int>(valid), 1);
-        const bool head = valid && !(lane > 0 && vprev && hprev + tok == reinterpret_cast<uint64_t>(hp));
-        const unsigned heads = __ballot_sync(kFull, head);
-        const int nvalid = __popc(__ballot_sync(kFull, valid));
-        const unsigned later = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
-        const int run = (later ? __ffs(later) - 1 : nvalid) - lane;
-        tab_dev[s * 32 + lane] = reinterpret_cast<uint64_t>(dp);
-        tab_host[s * 32 + lane] = reinterpret_cast<uint64_t>(hp);
-        tab_len[s * 32 + lane] = head ? run : 0;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tab_full[s]);
-      }
-      const int64_t j = k - ahead;
-      if (j >= 0 && j < my) {
-        const int sj = static_cast<int>(j % S);
-        mbar_wait(&data_full[sj], static_cast<uint32_t>((j / S) & 1));
-        const int run = tab_len[sj * 32 + lane];
-        if (run) bulk_s2g(reinterpret_cast<char*>(tab_host[sj * 32 + lane]), buf + static_cast<size_t>(sj) * SB + lane * tok,
-                          static_cast<uint32_t>(run * tok));
-        bulk_commit();
-      }
-    }
-    bulk_wait_all();
-  } else {
-    const int nvec = T * p.vpt;
-    for (int64_t k = warp - 1; k < my; k += kWsConsumers) {
-      const int s = static_cast<int>(k % S);
-      mbar_wait(&tab_full[s], static_cast<uint32_t>((k / S) & 1));
-      unsigned char* st = buf + static_cast<size_t>(s) * SB;
-      const uint64_t* tab = tab_dev + s * 32;
-      for (int base = 0; base < nvec; base += 32 * 8) {
-        int4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int vi = base + u * 32 + lane;
-          const int row = vec_row(p, vi < nvec ? vi : 0);
-          const uint64_t d = vi < nvec ? tab[row] : 0;
-          if (d) v[u] = ld_stream(reinterpret_cast<const void*>(row_vec<CONTIG>(d, vi - row * p.vpt, p, p.head_stride)));
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int vi = base + u * 32 + lane;
-          const int row = vec_row(p, vi < nvec ? vi : 0);
-          if (vi < nvec && tab[row]) st_shared_v4(st + row * tok + (vi - row * p.vpt) * 16, v[u]);
-        }
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&data_full[s]);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
 __global__ void validate_kernel(const __grid_constant__ ValidateParams v) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < v.ntok; g += stride) {
@@ -710,15 +585,10 @@ cudaError_t launch_ldg_fused(const FusedParams& p, int dir, int ctas, int thread
 
 cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s) {
   const bool contig = dev_contig(p);
-  if (warp_specialized) {
+  if (dir == 0 && warp_specialized) {
     const int smem = tma_buf_offset(p.tma_stages) + p.tma_stages * p.tma_stage_bytes;
-    if (dir == 0) {
-      if (contig) tma_ws_load_kernel<true><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
-      else tma_ws_load_kernel<false><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
-    } else {
-      if (contig) tma_ws_offload_kernel<true><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
-      else tma_ws_offload_kernel<false><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
-    }
+    if (contig) tma_ws_load_kernel<true><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
+    else tma_ws_load_kernel<false><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
     return cudaGetLastError();
   }
   if (dir == 0) return contig ? tma_launch<0, true>(p, ctas, s) : tma_launch<0, false>(p, ctas, s);
@@ -747,8 +617,6 @@ cudaError_t tma_prepare(int smem) {
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(tma_ws_load_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_ws_load_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(tma_ws_offload_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(tma_ws_offload_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;

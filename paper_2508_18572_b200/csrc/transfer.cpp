@@ -319,17 +319,13 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const bool tma = engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK;
   // TMA engine geometry: rows per stage (<= 32 lanes), stage bytes, depth
   if (tma) {
-    // the warp-specialised load ring is producer-bound per stage: larger stages (64 KiB) amortise
-    // it; the warp-specialised offload wants >= 3 stages (gather lookahead S-2) of 32 KiB
-    const bool ws_load = engine == STRATA_ENGINE_TMA && dir == 0;
-    const bool ws_off = engine == STRATA_ENGINE_TMA && dir == 1;
-    const int target = ws_load ? 2 * kTmaStageTarget : ws_off ? kTmaOffStageTarget : kTmaStageTarget;
+    // the warp-specialised ring is producer-bound per stage: larger stages (64 KiB) amortise it
+    const int target = engine == STRATA_ENGINE_TMA ? 2 * kTmaStageTarget : kTmaStageTarget;
     int rows = std::max(1, std::min(32, target / xp.tok_bytes));
     const int sb = rows * xp.tok_bytes;
     const int budget = p->tma_smem - strata::tma_header_bytes(strata::kTmaMaxStages);
     int stages = std::min(strata::kTmaMaxStages, budget / sb);
-    // the offload ring keeps one stage per gathering warp plus the store window (kernels.cu)
-    if (stages < (ws_off ? kTmaOffMinStages : 2)) {
+    if (stages < 2) {
       engine = STRATA_ENGINE_LDG;  // token rows too large for a 2-stage shared-memory ring
     } else {
       xp.tma_rows = rows;
