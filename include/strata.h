@@ -99,7 +99,7 @@ enum strata_engine {
                                  host_chunks_host is given and a layer moves >= 4 MiB (offloads then
                                  group layers into >= 128 KiB runs, see layer_group), else LDG */
   STRATA_ENGINE_LDG = 1,      /* warps, 16-byte LDG/STG register staging, warp index broadcast */
-  STRATA_ENGINE_TMA = 2,      /* load: one cp.async.bulk producer warp + 4 LSU consumer warps per CTA
+  STRATA_ENGINE_TMA = 2,      /* load: one cp.async.bulk producer warp + 15 LSU consumer warps per CTA
                                  over a shared-memory ring; offload: as STRATA_ENGINE_TMA_BULK */
   STRATA_ENGINE_TMA_BULK = 3, /* one warp per CTA, cp.async.bulk on both sides of the ring */
   STRATA_ENGINE_DMA = 4       /* copy-engine gather of whole page-first host runs (cudaMemcpyBatchAsync,
