@@ -204,7 +204,8 @@ def _config(args, g, q):
             "page_size": g.P, "host_chunk_tokens": g.C, "tokens_per_gpu": q.total_tokens,
             "requests": q.R, "fragmentation": args.frag, "bytes_per_step_per_gpu": g.kv * g.L * q.total_tokens * g.token_bytes,
             "l2": f"no flush: each step moves {g.kv * g.L * q.total_tokens * g.token_bytes / 2**30:.1f} GiB, "
-                  "far above the 126 MB L2", "parallelism": f"replicas x{args.gpus}"}
+                  "far above the 126 MB L2", "parallelism": (f"tp{args.gpus}: KV-head slices of one host tier" if g.host_heads > g.H
+                            else f"replicas x{args.gpus}")}
 
 
 def main():
@@ -236,11 +237,29 @@ def main():
     nb = g.num_pages * g.P * g.token_bytes
     k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
     v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)] if g.kv == 2 else k
+    # A tier holding every KV head (R28) is ONE file-backed mapping shared by the ranks when the
+    # node's /dev/shm can hold it (rank 0 creates and fills it); otherwise each rank keeps a copy.
+    shared, host_tier = None, "per-rank"
+    if g.host_heads > g.H and world > 1:
+        from paper_2508_18572_b200.shared_tier import SharedTier, free_bytes
+        ok = os.path.isdir("/dev/shm") and free_bytes("/dev/shm") > g.host_bytes + (1 << 30)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=red_dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()):
+            path = f"/dev/shm/strata_bench_tier_{os.environ.get('MASTER_PORT', '0')}"
+            if rank == 0:
+                shared = SharedTier(path, g.host_bytes, create=True)
+                kvgen.fill_random(shared.array, args.seed * 1000)
+            dist.barrier()
+            if rank != 0:
+                shared = SharedTier(path, g.host_bytes, create=False)
+            host_tier = f"one shared mapping for {world} ranks"
     pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
                        k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=g.num_pages,
                        num_chunks=g.num_chunks, device=local, host_heads=g.Ht, head_begin=g.h0,
-                       head_major=g.head_major)
-    kvgen.fill_random(pool.host, args.seed * 1000 + rank)
+                       head_major=g.head_major, host=shared.array if shared else None)
+    if shared is None:
+        kvgen.fill_random(pool.host, args.seed * 1000 + rank)
     reqs = st.Requests.from_kvgen(q, device=local)
     bytes_step = g.kv * g.L * q.total_tokens * g.token_bytes
     io = torch.cuda.Stream()
@@ -398,6 +417,7 @@ def main():
             "layer_group": args.layer_group or "default",
             "other_engines_gbs": others,
             "shared_gpu_test_mode": share or None,
+            "host_tier": host_tier,
             "zero_copy_kernels": zc,
             "per_layer_ms_last_step": [round(x, 4) for x in launch_ms],
         }
@@ -405,6 +425,9 @@ def main():
     pool.close()
     if world > 1:
         dist.barrier()
+    if shared is not None:
+        shared.close()
+    if world > 1:
         dist.destroy_process_group()
     return 0
 

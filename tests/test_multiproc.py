@@ -139,3 +139,69 @@ def test_control_plane_identical_across_tp_ranks():
         p.join(timeout=180)
         assert p.exitcode == 0
     assert q.get(timeout=10), "TP ranks' control planes diverged"
+
+
+def _shared_tier_worker(rank, world, port, path, out_q):
+    """Rank 0 creates a file-backed tier holding all heads (head-major, R28) and fills it; every
+    rank maps the SAME file (paper_2508_18572_b200.shared_tier) and loads its head slice."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import dataclasses
+
+        import kvgen
+        import oracle
+        from kvgen import Geometry
+        from paper_2508_18572_b200.shared_tier import SharedTier
+        oracle.build()
+        H_total = 4
+        full = Geometry(L=2, H=H_total, D=16, e=2, P=2, C=8, num_pages=64, num_chunks=12, Ht=H_total,
+                        head_major=True)
+        if rank == 0:
+            tier = SharedTier(path, full.host_bytes, create=True)
+            tier.array[:] = kvgen.random_bytes(kvgen.rng_for(5), full.host_bytes)
+        dist.barrier()
+        if rank != 0:
+            tier = SharedTier(path, full.host_bytes, create=False)
+        q = kvgen.make_requests(kvgen.rng_for(6), [40, 9], full.P, full.C, full.num_pages, full.num_chunks,
+                                offsets=True)
+        hs = kvgen.head_slice(rank, world, H_total)
+        g = dataclasses.replace(full, H=len(hs), h0=hs.start)
+        nb = g.num_pages * g.P * g.token_bytes
+        k = [np.zeros(nb, np.uint8) for _ in range(g.L)]
+        v = [np.zeros(nb, np.uint8) for _ in range(g.L)]
+        oracle.load(g, tier.array, k, v, q, 0, g.L)
+        parts = [torch.empty((2 * g.L, nb), dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(np.stack(k + v)))
+        dist.barrier()
+        if rank == 0:
+            nbf = full.num_pages * full.P * full.token_bytes
+            kf = [np.zeros(nbf, np.uint8) for _ in range(full.L)]
+            vf = [np.zeros(nbf, np.uint8) for _ in range(full.L)]
+            oracle.load(full, tier.array, kf, vf, q, 0, full.L)
+            hl = H_total // world
+            ok = all(np.array_equal(img.reshape(-1, H_total, full.D * full.e),
+                                    np.concatenate([p[i].numpy().reshape(-1, hl, full.D * full.e) for p in parts], 1))
+                     for i, img in enumerate(kf + vf))
+            out_q.put(bool(ok))
+        dist.barrier()
+        tier.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shared_tier_across_ranks_gloo(tmp_path):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    path = str(tmp_path / "tier.bin")
+    procs = [ctx.Process(target=_shared_tier_worker, args=(r, world, port, path, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    assert q.get(timeout=10), "head slices of the shared tier do not reassemble the full-head load"
+    assert not os.path.exists(path), "creator did not unlink the shared tier"
