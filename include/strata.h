@@ -103,7 +103,7 @@ enum strata_engine {
                                  over a shared-memory ring; offload: as STRATA_ENGINE_TMA_BULK */
   STRATA_ENGINE_TMA_BULK = 3, /* one warp per CTA, cp.async.bulk on both sides of the ring */
   STRATA_ENGINE_DMA = 4       /* copy-engine gather of whole page-first host runs (cudaMemcpyBatchAsync,
-                                 4 copy streams) into a double-buffered HBM staging ring + the LDG
+                                 one in-order copy stream) into a double-buffered HBM staging ring + the LDG
                                  kernel scattering staged rows to their pages (offload: the mirror).
                                  Needs strata_xfer.host_chunks_host. */
 };

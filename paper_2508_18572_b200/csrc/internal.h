@@ -140,8 +140,11 @@ struct strata_pool {
   int tma_smem = 0;
   strata_counters counters = {};
   // STRATA_ENGINE_DMA: double-buffered HBM staging ring, copy streams and their events (lazy)
-  static constexpr int kCopyStreams = 8;  // capacity; `ncs` are used (env STRATA_COPY_STREAMS, default 4)
-  int ncs = 4;
+  // capacity; `ncs` are used (env STRATA_COPY_STREAMS).  Default 1: with the per-piece barrier one
+  // in-order copy stream beats 2-8 streams on every config and in both directions
+  // (profiles/r01/copy_streams: Llama-8B 55.36 vs 54.37 GB/s at 1 vs 4; bidirectional 101 vs 91)
+  static constexpr int kCopyStreams = 8;
+  int ncs = 1;
   char* stage[2] = {nullptr, nullptr};
   size_t stage_bytes = 0;             // bytes per staging slot
   int32_t* slot_ids = nullptr;        // device iota [0, slot_cap): chunk index of each staging slot

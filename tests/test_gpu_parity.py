@@ -180,13 +180,16 @@ def test_dma_engine_multi_piece(direction, group):
         c.close()
 
 
-@pytest.mark.parametrize("edge,ordered", [("1", "0"), ("1", "1"), ("4", "1"), ("16", "0")])
+@pytest.mark.parametrize("edge,ordered,streams", [("1", "0", "4"), ("1", "1", "4"), ("4", "1", "4"), ("16", "0", "3"),
+                                                  ("4", "1", "1"), ("4", "0", "8")])
 @pytest.mark.parametrize("direction", ["load", "offload"])
-def test_dma_engine_piece_schedule(direction, edge, ordered, monkeypatch):
+def test_dma_engine_piece_schedule(direction, edge, ordered, streams, monkeypatch):
     """The DMA engine's piece schedule (edge pieces of the first / last layer, the per-piece copy
-    barrier) changes only timing: the result stays the oracle's and layer events stay ordered."""
+    barrier, the number of copy streams) changes only timing: the result stays the oracle's and
+    layer events stay ordered."""
     monkeypatch.setenv("STRATA_DMA_EDGE_SPLIT", edge)
     monkeypatch.setenv("STRATA_DMA_ORDERED", ordered)
+    monkeypatch.setenv("STRATA_COPY_STREAMS", streams)
     g = Geometry(4, 8, 128, 2, 1, 64, 40960, 560)
     rng = kvgen.rng_for(22)
     q = kvgen.make_requests(rng, [21000, 12000, 300], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
