@@ -139,7 +139,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 12.0):
+def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 10.0):
     """The oracle as it stands (oracle/oracle.c, OpenMP over all host cores), timed on this box on the
     same workload: DRAM->DRAM into host images of the device pool (SURVEY.md §8d "Oracle timing")."""
     import oracle
@@ -153,7 +153,8 @@ def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 12.0):
     bytes_per = g.kv * g.L * q.total_tokens * g.token_bytes
     times = []
     t_start = time.time()
-    while not times or (time.time() - t_start < budget_s and len(times) < 5):
+    # a bounded sample of ~10 s of CPU work (at least 3 full loads, at most 200)
+    while len(times) < 3 or (time.time() - t_start < budget_s and len(times) < 200):
         t0 = time.perf_counter()
         oracle.load(g, host, k, v, q, 0, g.L, nthreads=threads)
         times.append(time.perf_counter() - t0)
