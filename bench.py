@@ -36,7 +36,7 @@ METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 ENGINE_NAMES = {0: "default", 1: "ldg", 2: "tma", 3: "tma_bulk", 4: "dma"}
 SM_ZERO_COPY_CEILING = 51.44   # GB/s, profiles/r01/probe.jsonl: SM-issued host reads, best of the sweep
 PATH_DESC = {
-    "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (cudaMemcpyBatchAsync, 4 streams) "
+    "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (cudaMemcpyBatchAsync on one in-order copy stream) "
            "into an HBM staging slot + ldg_kernel scatter to the pages; one event per layer",
     "ldg": "ldg_kernel, zero-copy LDG/STG from mapped host memory, one launch + event per layer",
     "tma": "tma_ws_load_kernel, zero-copy cp.async.bulk ring, one launch + event per layer",
