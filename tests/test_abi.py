@@ -25,6 +25,38 @@ def test_exports_every_declared_symbol(lib):
     assert lib.strata_version() >= 100
 
 
+def test_ctypes_structs_match_the_c_compiler(tmp_path):
+    """sizeof / offsetof of every field of every struct in include/*.h as gcc lays them out, against
+    the ctypes mirrors the binding passes across the ABI."""
+    import os
+    import subprocess
+
+    from paper_2508_18572_b200 import ctl, disk
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    structs = [("strata_pool_desc", PoolDesc), ("strata_xfer", Xfer), ("strata_counters", _lib.Counters),
+               ("strata_ctl_desc", ctl.CtlDesc), ("strata_ctl_match_t", ctl.Match), ("strata_ctl_round", ctl.Round),
+               ("strata_ctl_plan", ctl.Plan), ("strata_ctl_stats", ctl.Stats), ("strata_disk_desc", disk.DiskDesc)]
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "strata.h"', '#include "strata_ctl.h"',
+             '#include "strata_disk.h"', "int main(void) {"]
+    for cname, cls in structs:
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c99", "-I", inc, "-o", str(exe), str(src)])
+    got = {}
+    for ln in subprocess.check_output([str(exe)], text=True).splitlines():
+        c, f, v = ln.split()
+        got[(c, f)] = int(v)
+    for cname, cls in structs:
+        assert got[(cname, "sizeof")] == ctypes.sizeof(cls), cname
+        for f, _ in cls._fields_:
+            assert got[(cname, f)] == getattr(cls, f).offset, (cname, f)
+
+
 def test_struct_layouts_match_header(lib):
     # int32 x8 then pointers/int64 (see include/strata.h); 8-byte aligned, no padding surprises
     assert ctypes.sizeof(PoolDesc) == 8 * 4 + 2 * 8 + 4 * 8 + 8 + 8 + 2 * 4   # + host_heads, head_begin
