@@ -157,7 +157,8 @@ typedef struct {
   int32_t reserved;
 } strata_xfer;
 
-/* Register the host tier and bind it to the device pool described by *d.
+/* Register the host tier and bind it to the device pool described by *d ("CPU registered pinned
+ * memory" the I/O kernels read directly, §4.2; a node-sized pinned tier).
  * Host memory: if d->host_base != NULL it must hold num_chunks*chunk_bytes bytes, 16-byte aligned;
  * the library page-locks and maps it (cudaHostRegisterMapped|Portable) and unregisters it in
  * strata_unregister_host_pool; the caller keeps ownership.  If NULL, the library allocates it
@@ -173,7 +174,9 @@ int strata_unregister_host_pool(strata_pool_t p);
 /* Host address and size of the registered host tier (for filling / reading it on the CPU). */
 int strata_host_pool_ptr(strata_pool_t p, void** host_base, size_t* bytes);
 
-/* LOAD: for every request r, token i < num_tokens[r], layer l in [l0,l1), kv, head: copy D*e bytes
+/* LOAD (§4.2 GPU-assisted I/O; the page-first -> layer-first transform of
+ * PAPER.md:284-290 §4.2.1; page-table indirection PAPER.md:653-655 §2.2): for every request r,
+ * token i < num_tokens[r], layer l in [l0,l1), kv, head: copy D*e bytes
  * from the host tier to the device pool (addresses in the LAYOUTS block).  Enqueued on `stream`;
  * layers are processed in increasing order and event (ticket, l) completes once every byte of
  * layer l of this call is in the device pool.  n = 0 or l0 = l1 is a successful no-op that still
