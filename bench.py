@@ -283,9 +283,12 @@ def main():
     with ClockSampler(local) as clocks:
         start.record(io)
         last = None
+        host_s = 0.0   # CPU time inside the strata_load calls (submission only; they never block)
         for i in range(args.steps):
             marks[i].record(io)
+            h0 = time.perf_counter()
             last = step()
+            host_s += time.perf_counter() - h0
         marks[-1].record(io)
         end.record(io)
         barrier()
@@ -421,6 +424,7 @@ def main():
             "host_tier": host_tier,
             "zero_copy_kernels": zc,
             "per_layer_ms_last_step": [round(x, 4) for x in launch_ms],
+            "host_submit_ms_per_step": round(host_s / args.steps * 1e3, 3),
         }
         print(json.dumps(out), flush=True)
     pool.close()
