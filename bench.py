@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--impl", default="strata", choices=["strata", "reference"])
     ap.add_argument("--config", default="llama8b_32k", choices=list(kvgen.CONFIGS))
     ap.add_argument("--page-size", type=int, default=None)
+    ap.add_argument("--chunk-tokens", type=int, default=None,
+                    help="host chunk size C (the host tier keeps the same token capacity)")
     ap.add_argument("--engine", type=int, default=0, help="0 default, 1 LDG, 2 TMA")
     ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--layer-group", type=int, default=0, help="DMA engine: layers per copy run (0 = library default)")
@@ -72,6 +74,8 @@ def workload(args, rank: int, world: int):
     """Per-rank geometry + request tables (replicas of the config; the TP config is already the
     per-rank head slice)."""
     g = kvgen.geometry(args.config, P=args.page_size)
+    if args.chunk_tokens and args.chunk_tokens != g.C:
+        g = dataclasses.replace(g, C=args.chunk_tokens, num_chunks=-(-g.num_chunks * g.C // args.chunk_tokens))
     if g.host_heads > g.H:   # a shared tier holding every KV head: this rank moves head slice `rank`
         g = dataclasses.replace(g, h0=(rank % (g.host_heads // g.H)) * g.H)
     n = kvgen.CONFIGS[args.config]["n"]
