@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--layer-group", type=int, default=0, help="DMA engine: layers per copy run (0 = library default)")
     ap.add_argument("--frag", default="perm", choices=["perm", "churn"])
+    ap.add_argument("--chunk-frag", default="perm", choices=["perm", "identity"],
+                    help="host chunk lists: a random permutation of the tier, or consecutive chunks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     return ap.parse_args()
@@ -80,10 +82,7 @@ def workload(args, rank: int, world: int):
         g = dataclasses.replace(g, h0=(rank % (g.host_heads // g.H)) * g.H)
     n = kvgen.CONFIGS[args.config]["n"]
     rng = kvgen.rng_for(args.seed * 1000 + rank)
-    if args.frag == "perm":
-        q = kvgen.make_requests(rng, n, g.P, g.C, g.num_pages, g.num_chunks)
-    else:
-        q = kvgen.make_requests(rng, n, g.P, g.C, g.num_pages, g.num_chunks, frag="churn")
+    q = kvgen.make_requests(rng, n, g.P, g.C, g.num_pages, g.num_chunks, frag=args.frag, chunk_frag=args.chunk_frag)
     return g, q
 
 
@@ -207,7 +206,7 @@ def _config(args, g, q):
             "kv_buffers_per_layer": g.kv, "host_heads": g.host_heads, "head_begin": g.h0,
             "host_layout": "head-major" if g.head_major else "token-major",
             "page_size": g.P, "host_chunk_tokens": g.C, "tokens_per_gpu": q.total_tokens,
-            "requests": q.R, "fragmentation": args.frag, "bytes_per_step_per_gpu": g.kv * g.L * q.total_tokens * g.token_bytes,
+            "requests": q.R, "fragmentation": args.frag, "host_chunk_order": args.chunk_frag, "bytes_per_step_per_gpu": g.kv * g.L * q.total_tokens * g.token_bytes,
             "l2": f"no flush: each step moves {g.kv * g.L * q.total_tokens * g.token_bytes / 2**30:.1f} GiB, "
                   "far above the 126 MB L2", "parallelism": (f"tp{args.gpus}: KV-head slices of one host tier" if g.host_heads > g.H
                             else f"replicas x{args.gpus}")}

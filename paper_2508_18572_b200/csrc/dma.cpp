@@ -93,9 +93,21 @@ void free_dma(strata_pool* p) {
   }
 }
 
-// Submit a copy list over the pool's copy streams (contiguous shares, one batch call each).
+// A run of k chunks with consecutive host ids: layer block j of each sits chunk_bytes after the
+// previous one on the host and one staging slot after it on the device, so the run is ONE strided
+// copy (cudaMemcpy2DAsync) instead of k.  Host allocators that hand out chunks in order (the
+// control plane's free lists, a fresh tier) make such runs the common case.
+struct Copy2D {
+  void* dst;
+  size_t dpitch;
+  const void* src;
+  size_t spitch, width, height;
+};
+
+// Submit a copy list over the pool's copy streams (contiguous shares, one batch call each); the
+// strided runs go to the first stream.
 static cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sz,
-                          int dir, int slot) {
+                          const std::vector<Copy2D>& c2d, int dir, int slot) {
   cudaMemcpyAttributes attr;
   memset(&attr, 0, sizeof attr);
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -110,6 +122,10 @@ static cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::v
   cudaError_t e0 = cudaStreamIsCapturing(p->cs[0], &cap);
   if (e0 != cudaSuccess) return e0;
   const cudaMemcpyKind kind = dir == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  for (const Copy2D& r : c2d) {
+    cudaError_t e = cudaMemcpy2DAsync(r.dst, r.dpitch, r.src, r.spitch, r.width, r.height, kind, p->cs[0]);
+    if (e != cudaSuccess) return e;
+  }
   for (int c = 0; c < ns; ++c) {
     const size_t lo = n * c / ns, hi = n * (c + 1) / ns;
     if (hi > lo && cap == cudaStreamCaptureStatusActive) {
@@ -219,6 +235,9 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
   std::vector<void*> dst, src;
   std::vector<size_t> sz;
+  std::vector<Copy2D> c2d;
+  bool strided = true;   // env STRATA_DMA_STRIDED=0: one copy per chunk (A/B only)
+  if (const char* v = getenv("STRATA_DMA_STRIDED")) strided = atoi(v) != 0;
   int64_t i = 0;
   int last_slot = 0;
   auto layer_event = [&](int32_t l) { return p->events[size_t(slot_ev) * (L + 1) + 1 + l]; };
@@ -233,9 +252,29 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
       dst.clear();
       src.clear();
       sz.clear();
+      c2d.clear();
+      auto host_chunk = [&](size_t j) {
+        const ChunkPos& c = pos[pc.first + j];
+        return int64_t(x->host_chunks_host[x->chunk_start[c.req] + c.cq]);
+      };
+      auto full = [&](size_t j) { return pos[pc.first + j].lo == 0 && pos[pc.first + j].cnt == C; };
       for (size_t j = 0; j < pc.count; ++j) {
         const ChunkPos& cp = pos[pc.first + j];
-        const int64_t hc = x->host_chunks_host[x->chunk_start[cp.req] + cp.cq];
+        const int64_t hc = host_chunk(j);
+        if (strided && !hm && full(j)) {   // token-major full chunks: extend over consecutive host ids
+          size_t k = 1;
+          while (j + k < pc.count && full(j + k) && host_chunk(j + k) == hc + int64_t(k)) ++k;
+          if (k >= 2) {
+            char* h0p = p->host + hc * p->chunk_bytes + int64_t(lg) * int64_t(unit);
+            char* d0p = stage + j * gunit;
+            const size_t width = size_t(gl) * unit;
+            if (dir == 0) c2d.push_back({d0p, gunit, h0p, size_t(p->chunk_bytes), width, k});
+            else c2d.push_back({h0p, size_t(p->chunk_bytes), d0p, gunit, width, k});
+            p->counters.dma_copies += 1;
+            j += k - 1;
+            continue;
+          }
+        }
         char* h = p->host + hc * p->chunk_bytes + int64_t(lg) * int64_t(unit);
         char* d = stage + j * gunit;
         auto add = [&](int64_t off, int64_t bytes) {
@@ -326,7 +365,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
             for (int cj = 0; cj < ncs; ++cj)
               if (cj != ci && (e = cudaStreamWaitEvent(p->cs[ci], p->ev_copy[slot ^ 1][cj], 0)))
                 return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        if ((e = submit_copies(p, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
         for (int ci = 0; ci < ncs; ++ci)
           if ((e = cudaStreamWaitEvent(s, p->ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = launch_group(0))) return cuda_fail(e, "scatter kernel launch");
@@ -340,7 +379,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
         if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
         for (int ci = 0; ci < ncs; ++ci)
           if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, dst, src, sz, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        if ((e = submit_copies(p, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
       }
       p->counters.dma_copies += static_cast<int64_t>(dst.size());
       last_slot = slot;

@@ -210,6 +210,36 @@ def test_dma_engine_piece_schedule(direction, edge, ordered, streams, monkeypatc
         c.close()
 
 
+@pytest.mark.parametrize("strided", ["1", "0"])
+@pytest.mark.parametrize("group", [1, 3])
+@pytest.mark.parametrize("direction", ["load", "offload"])
+def test_dma_strided_chunk_runs(direction, group, strided, monkeypatch):
+    """Consecutive host chunk ids become one strided copy per run (cudaMemcpy2DAsync): requests
+    with partial first / last chunks, runs broken by the request boundary and by a permuted tail,
+    layer groups; the result stays the oracle's."""
+    monkeypatch.setenv("STRATA_DMA_STRIDED", strided)
+    g = Geometry(5, 8, 128, 2, 1, 64, 40960, 700)
+    rng = kvgen.rng_for(23)
+    q = kvgen.make_requests(rng, [20000, 9000, 130], g.P, g.C, g.num_pages, g.num_chunks, offsets=True,
+                            chunk_frag="identity")
+    hc = q.host_chunks.copy()
+    hc[-40:] = rng.permutation(hc[-40:])          # a permuted tail: short runs and singles
+    q.host_chunks = hc
+    c = GpuCase(g, q, dev_fill="canary" if direction == "load" else "random")
+    try:
+        if direction == "load":
+            c.pool.load(c.reqs, 0, 5, engine=st.STRATA_ENGINE_DMA, layer_group=group)
+            _sync()
+            c.check_load(0, 5)
+        else:
+            before = c.pool.host.copy()
+            c.pool.offload(c.reqs, 0, 5, engine=st.STRATA_ENGINE_DMA, layer_group=group)
+            _sync()
+            assert np.array_equal(c.pool.host, c.expected_offload(before, 0, 5))
+    finally:
+        c.close()
+
+
 def test_dma_engine_needs_host_list():
     g = kvgen.geometry("tiny")
     q = kvgen.make_requests(kvgen.rng_for(0), [64], g.P, g.C, g.num_pages, g.num_chunks)

@@ -15,7 +15,8 @@ import paper_2508_18572_b200 as st  # noqa: E402
 
 def main():
     g = kvgen.geometry("llama8b_32k")
-    q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks)
+    chunk_frag = sys.argv[1] if len(sys.argv) > 1 else "perm"
+    q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks, chunk_frag=chunk_frag)
     nb = g.num_pages * g.P * g.token_bytes
     k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
     v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
@@ -33,7 +34,9 @@ def main():
             t = pool.load(reqs, stream=io, engine=eng)
             t1 = time.perf_counter()
             ms = pool.layer_elapsed_ms(t, g.L - 1)
-            print(json.dumps({"engine": eng, "copy_streams": os.environ.get("STRATA_COPY_STREAMS", "default"),
+            print(json.dumps({"engine": eng, "chunk_order": chunk_frag,
+                              "strided": os.environ.get("STRATA_DMA_STRIDED", "default"),
+                              "copy_streams": os.environ.get("STRATA_COPY_STREAMS", "default"),
                               "call_ms": round((t1 - t0) * 1e3, 3), "device_ms": round(ms, 3)}), flush=True)
             torch.cuda.synchronize()
     pool.close()
