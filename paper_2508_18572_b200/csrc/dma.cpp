@@ -261,16 +261,23 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
       for (size_t j = 0; j < pc.count; ++j) {
         const ChunkPos& cp = pos[pc.first + j];
         const int64_t hc = host_chunk(j);
-        if (strided && !hm && full(j)) {   // token-major full chunks: extend over consecutive host ids
+        if (strided && full(j)) {   // full chunks: extend over consecutive host ids
           size_t k = 1;
           while (j + k < pc.count && full(j + k) && host_chunk(j + k) == hc + int64_t(k)) ++k;
           if (k >= 2) {
-            char* h0p = p->host + hc * p->chunk_bytes + int64_t(lg) * int64_t(unit);
-            char* d0p = stage + j * gunit;
-            const size_t width = size_t(gl) * unit;
-            if (dir == 0) c2d.push_back({d0p, gunit, h0p, size_t(p->chunk_bytes), width, k});
-            else c2d.push_back({h0p, size_t(p->chunk_bytes), d0p, gunit, width, k});
-            p->counters.dma_copies += 1;
+            // token-major: the group's layers of a chunk are one block; head-major: one block per
+            // head of this GPU (the layers of head h0+hh, [L][KV][C][D] inside the chunk)
+            const int64_t lay = nkv * C * hb;
+            const int nblk = hm ? int(Hl) : 1;
+            for (int b = 0; b < nblk; ++b) {
+              char* h0p = p->host + hc * p->chunk_bytes +
+                          (hm ? (h0 + b) * p->host_head_stride + int64_t(lg) * lay : int64_t(lg) * int64_t(unit));
+              char* d0p = stage + j * gunit + (hm ? size_t(b) * G * lay : 0);
+              const size_t width = hm ? size_t(gl) * lay : size_t(gl) * unit;
+              if (dir == 0) c2d.push_back({d0p, gunit, h0p, size_t(p->chunk_bytes), width, k});
+              else c2d.push_back({h0p, size_t(p->chunk_bytes), d0p, gunit, width, k});
+              p->counters.dma_copies += 1;
+            }
             j += k - 1;
             continue;
           }

@@ -1,0 +1,71 @@
+"""Several operations of ONE pool in flight at once on different streams: a load and
+an offload (both directions of the link at once), two loads, two offloads — every engine pairing,
+each result bit-exact against the oracle.  The operations touch disjoint device slots and host
+chunks, so each one's expected image is independent of the other's timing."""
+import numpy as np
+import pytest
+
+import kvgen
+import oracle
+from kvgen import Geometry
+from tests.helpers import CANARY
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2508_18572_b200 as st  # noqa: E402
+
+DMA, LDG, TMA = st.STRATA_ENGINE_DMA, st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_TMA
+
+
+def _setup(n=20000, L=4, seed=31):
+    # two disjoint halves of the device pool and of the host tier
+    g = Geometry(L, 8, 128, 2, 1, 64, 2 * 25000, 2 * 400)
+    rng = kvgen.rng_for(seed)
+    half_p, half_c = g.num_pages // 2, g.num_chunks // 2
+    qa = kvgen.make_requests(rng, [n, 777], g.P, g.C, half_p, half_c, offsets=True)
+    qb = kvgen.make_requests(rng, [n - 5000, 1500], g.P, g.C, half_p, half_c, offsets=True)
+    qb.dev_pages = (qb.dev_pages + half_p).astype(np.int32)
+    qb.host_chunks = (qb.host_chunks + half_c).astype(np.int32)
+    nb = g.num_pages * g.P * g.token_bytes
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    k = [torch.randint(0, 256, (nb,), dtype=torch.uint8, device="cuda", generator=gen) for _ in range(g.L)]
+    v = [torch.randint(0, 256, (nb,), dtype=torch.uint8, device="cuda", generator=gen) for _ in range(g.L)]
+    pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+    pool.host[:] = kvgen.random_bytes(rng, g.host_bytes)
+    return g, qa, qb, k, v, pool
+
+
+@pytest.mark.parametrize("ea,eb", [(DMA, DMA), (DMA, LDG), (LDG, DMA), (LDG, LDG), (TMA, DMA)])
+@pytest.mark.parametrize("kinds", [("load", "offload"), ("load", "load"), ("offload", "offload")])
+def test_two_operations_in_flight(kinds, ea, eb):
+    g, qa, qb, k, v, pool = _setup()
+    try:
+        host0 = pool.host.copy()
+        dev0k = [t.cpu().numpy() for t in k]
+        dev0v = [t.cpu().numpy() for t in v]
+        sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+        torch.cuda.synchronize()
+        for kind, q, eng, s in ((kinds[0], qa, ea, sa), (kinds[1], qb, eb, sb)):
+            op = pool.load if kind == "load" else pool.offload
+            op(st.Requests.from_kvgen(q), stream=s, engine=eng)
+        torch.cuda.synchronize()
+        # expected: apply both (disjoint) operations to the pre-states with the oracle
+        ek, ev_ = [a.copy() for a in dev0k], [a.copy() for a in dev0v]
+        eh = host0.copy()
+        for kind, q in ((kinds[0], qa), (kinds[1], qb)):
+            if kind == "load":
+                oracle.load(g, host0, ek, ev_, q, 0, g.L)
+            else:
+                oracle.offload(g, eh, dev0k, dev0v, q, 0, g.L)
+        for l in range(g.L):
+            assert np.array_equal(k[l].cpu().numpy(), ek[l]), f"K layer {l}"
+            assert np.array_equal(v[l].cpu().numpy(), ev_[l]), f"V layer {l}"
+        assert np.array_equal(pool.host, eh), "host tier"
+    finally:
+        pool.close()

@@ -134,3 +134,32 @@ def test_llama70b_tp8_shared_tier_bench_config():
         c.check_load(0, g.L, layers=[0, 41, 79])
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("group", [1, 2])
+@pytest.mark.parametrize("H,Ht,h0", [(1, 8, 6), (2, 4, 1), (4, 4, 0)])
+def test_head_major_strided_runs_dma(H, Ht, h0, group):
+    """Consecutive host chunks of a head-major tier move as one strided copy per head and run
+    (copy engines), with partial first / last chunks and a permuted tail; both directions."""
+    g = Geometry(L=3, H=H, D=128, e=2, P=1, C=64, num_pages=12000, num_chunks=200, Ht=Ht, h0=h0,
+                 head_major=True)
+    rng = kvgen.rng_for(95)
+    q = kvgen.make_requests(rng, [7000, 3000], g.P, g.C, g.num_pages, g.num_chunks, offsets=True,
+                            chunk_frag="identity")
+    hc = q.host_chunks.copy()
+    hc[-20:] = rng.permutation(hc[-20:])
+    q.host_chunks = hc
+    c = GpuCase(g, q, seed=5)
+    try:
+        c.pool.load(c.reqs, engine=st.STRATA_ENGINE_DMA, layer_group=group)
+        torch.cuda.synchronize()
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_DMA
+        c.check_load(0, g.L)
+        before = c.pool.host.copy()
+        for t in c.k + c.v:
+            t.copy_(torch.randint(0, 256, t.shape, dtype=torch.uint8, device="cuda"))
+        c.pool.offload(c.reqs, engine=st.STRATA_ENGINE_DMA, layer_group=group)
+        torch.cuda.synchronize()
+        assert np.array_equal(c.pool.host, c.expected_offload(before, 0, g.L))
+    finally:
+        c.close()
