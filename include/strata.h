@@ -46,7 +46,9 @@
  * Asynchronous kernel faults surface as STRATA_ERR_CUDA on a later call.
  *
  * THREADING: a pool handle is single-writer (one thread at a time); distinct handles are
- * independent.
+ * independent.  Operations of one handle may be in flight at once on different streams (e.g. a
+ * load and an offload: both directions of the link); the library orders their use of its internal
+ * staging buffers, the caller keeps their destinations disjoint (tests/test_gpu_concurrent.py).
  */
 #ifndef STRATA_H
 #define STRATA_H

@@ -40,30 +40,30 @@ constexpr size_t kStageTarget = size_t(128) << 20;
 constexpr int kDefaultCtasScatter = 8;
 constexpr size_t kDmaMinEdgePiece = size_t(16) << 20;   // edge pieces are not cut below this
 
-static int ensure_dma(strata_pool* p, size_t slot_bytes, int64_t slots) {
+static int ensure_dma(strata_pool* p, strata_pool::DmaDir& D, size_t slot_bytes, int64_t slots) {
   cudaError_t e;
-  if (!p->cs[0]) {
+  if (!D.cs[0]) {
     if (const char* v = getenv("STRATA_COPY_STREAMS"))
-      p->ncs = std::max(1, std::min(strata_pool::kCopyStreams, atoi(v)));
-    for (auto& c : p->cs)
+      D.ncs = std::max(1, std::min(strata_pool::kCopyStreams, atoi(v)));
+    for (auto& c : D.cs)
       if ((e = cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking))) return cuda_fail(e, "cudaStreamCreate");
-    if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+    if ((e = cudaEventCreateWithFlags(&D.ev_fork, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
     for (int s = 0; s < 2; ++s) {
-      if ((e = cudaEventCreateWithFlags(&p->ev_slot[s], cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
-      for (auto& ev : p->ev_copy[s])
+      if ((e = cudaEventCreateWithFlags(&D.ev_slot[s], cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+      for (auto& ev : D.ev_copy[s])
         if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
     }
   }
-  if (p->stage_bytes < slot_bytes) {
-    for (auto& b : p->stage) {
+  if (D.stage_bytes < slot_bytes) {
+    for (auto& b : D.stage) {
       if (b) cudaFree(b);
       b = nullptr;
     }
-    p->stage_bytes = 0;
-    for (auto& b : p->stage)
+    D.stage_bytes = 0;
+    for (auto& b : D.stage)
       if ((e = cudaMalloc(&b, slot_bytes))) return fail(STRATA_ERR_OOM, "cudaMalloc(staging %zu): %s", slot_bytes,
                                                         cudaGetErrorString(e));
-    p->stage_bytes = slot_bytes;
+    D.stage_bytes = slot_bytes;
   }
   if (p->slot_cap < slots) {
     if (p->slot_ids) cudaFree(p->slot_ids);
@@ -80,16 +80,18 @@ static int ensure_dma(strata_pool* p, size_t slot_bytes, int64_t slots) {
 }
 
 void free_dma(strata_pool* p) {
-  for (auto& b : p->stage)
-    if (b) cudaFree(b);
   if (p->slot_ids) cudaFree(p->slot_ids);
-  for (auto& c : p->cs)
-    if (c) cudaStreamDestroy(c);
-  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
-  for (int s = 0; s < 2; ++s) {
-    if (p->ev_slot[s]) cudaEventDestroy(p->ev_slot[s]);
-    for (auto& ev : p->ev_copy[s])
-      if (ev) cudaEventDestroy(ev);
+  for (auto& D : p->dma) {
+    for (auto& b : D.stage)
+      if (b) cudaFree(b);
+    for (auto& c : D.cs)
+      if (c) cudaStreamDestroy(c);
+    if (D.ev_fork) cudaEventDestroy(D.ev_fork);
+    for (int s = 0; s < 2; ++s) {
+      if (D.ev_slot[s]) cudaEventDestroy(D.ev_slot[s]);
+      for (auto& ev : D.ev_copy[s])
+        if (ev) cudaEventDestroy(ev);
+    }
   }
 }
 
@@ -106,7 +108,7 @@ struct Copy2D {
 
 // Submit a copy list over the pool's copy streams (contiguous shares, one batch call each); the
 // strided runs go to the first stream.
-static cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sz,
+static cudaError_t submit_copies(strata_pool* p, strata_pool::DmaDir& D, std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sz,
                           const std::vector<Copy2D>& c2d, int dir, int slot) {
   cudaMemcpyAttributes attr;
   memset(&attr, 0, sizeof attr);
@@ -116,30 +118,30 @@ static cudaError_t submit_copies(strata_pool* p, std::vector<void*>& dst, std::v
   attr.dstLocHint.type = dir == 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
   attr.dstLocHint.id = dir == 0 ? p->d.device : 0;
   const size_t n = dst.size();
-  const int ns = p->ncs;
+  const int ns = D.ncs;
   // cudaMemcpyBatchAsync refuses stream capture; under capture the copies become plain memcpy nodes
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaError_t e0 = cudaStreamIsCapturing(p->cs[0], &cap);
+  cudaError_t e0 = cudaStreamIsCapturing(D.cs[0], &cap);
   if (e0 != cudaSuccess) return e0;
   const cudaMemcpyKind kind = dir == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
   for (const Copy2D& r : c2d) {
-    cudaError_t e = cudaMemcpy2DAsync(r.dst, r.dpitch, r.src, r.spitch, r.width, r.height, kind, p->cs[0]);
+    cudaError_t e = cudaMemcpy2DAsync(r.dst, r.dpitch, r.src, r.spitch, r.width, r.height, kind, D.cs[0]);
     if (e != cudaSuccess) return e;
   }
   for (int c = 0; c < ns; ++c) {
     const size_t lo = n * c / ns, hi = n * (c + 1) / ns;
     if (hi > lo && cap == cudaStreamCaptureStatusActive) {
       for (size_t i = lo; i < hi; ++i) {
-        cudaError_t e = cudaMemcpyAsync(dst[i], src[i], sz[i], kind, p->cs[c]);
+        cudaError_t e = cudaMemcpyAsync(dst[i], src[i], sz[i], kind, D.cs[c]);
         if (e != cudaSuccess) return e;
       }
     } else if (hi > lo) {
       size_t idx = 0, fail_idx = 0;
       cudaError_t e = cudaMemcpyBatchAsync(dst.data() + lo, src.data() + lo, sz.data() + lo, hi - lo, &attr, &idx, 1,
-                                           &fail_idx, p->cs[c]);
+                                           &fail_idx, D.cs[c]);
       if (e != cudaSuccess) return e;
     }
-    cudaError_t e = cudaEventRecord(p->ev_copy[slot][c], p->cs[c]);
+    cudaError_t e = cudaEventRecord(D.ev_copy[slot][c], D.cs[c]);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -209,7 +211,8 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   if (const char* v = getenv("STRATA_DMA_EDGE_SPLIT")) edge = std::max(1, atoi(v));
   const size_t edge_cap = std::min(per_piece, std::max<size_t>({1, per_piece / size_t(edge), kDmaMinEdgePiece / gunit}));
   const std::vector<Piece> edge_pieces = edge_cap < per_piece ? make_pieces(edge_cap) : pieces;
-  int rc = ensure_dma(p, per_piece * gunit, static_cast<int64_t>(per_piece));
+  strata_pool::DmaDir& D = p->dma[dir];
+  int rc = ensure_dma(p, D, per_piece * gunit, static_cast<int64_t>(per_piece));
   if (rc) return rc;
 
   cudaError_t e;
@@ -230,15 +233,16 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   xp.host_head_off = 0;
   xp.host_head_stride = hm ? int64_t(G) * nkv * C * hb : hb;
 
-  if ((e = cudaEventRecord(p->ev_fork, s))) return cuda_fail(e, "cudaEventRecord");
-  for (int ci = 0; ci < p->ncs; ++ci)
-    if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+  if ((e = cudaEventRecord(D.ev_fork, s))) return cuda_fail(e, "cudaEventRecord");
+  for (int ci = 0; ci < D.ncs; ++ci)
+    if ((e = cudaStreamWaitEvent(D.cs[ci], D.ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
   std::vector<void*> dst, src;
   std::vector<size_t> sz;
   std::vector<Copy2D> c2d;
   bool strided = true;   // env STRATA_DMA_STRIDED=0: one copy per chunk (A/B only)
   if (const char* v = getenv("STRATA_DMA_STRIDED")) strided = atoi(v) != 0;
-  int64_t i = 0;
+  int64_t i = 0;                 // pieces of this operation
+  uint64_t& seq = D.seq;          // pieces of this direction, across operations
   int last_slot = 0;
   auto layer_event = [&](int32_t l) { return p->events[size_t(slot_ev) * (L + 1) + 1 + l]; };
   for (int32_t lg = x->layer_begin; lg < x->layer_end; lg += G) {
@@ -246,8 +250,8 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     const std::vector<Piece>& gp = (lg == x->layer_begin || lg + G >= x->layer_end) ? edge_pieces : pieces;
     for (const Piece& pc : gp) {
       const bool last_piece = &pc == &gp.back();
-      const int slot = static_cast<int>(i & 1);
-      char* stage = p->stage[slot];
+      const int slot = static_cast<int>(seq & 1);
+      char* stage = D.stage[slot];
       // copy list of this piece for layers [lg, lg+gl) (host <-> staging slot)
       dst.clear();
       src.clear();
@@ -357,12 +361,12 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
         }
         return cudaSuccess;
       };
-      const int ncs = p->ncs;
+      const int ncs = D.ncs;
       if (dir == 0) {
         // copies into the slot (after its previous scatter), then the scatters on the caller's stream
-        if (i >= 2)
+        if (seq >= 2)
           for (int ci = 0; ci < ncs; ++ci)
-            if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+            if ((e = cudaStreamWaitEvent(D.cs[ci], D.ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         // piece barrier: no copy stream starts piece i before every stream has finished piece i-1.
         // Without it the copy engines are not served fairly, a lagging stream's share of layer l
         // completes together with layer l+1 and the layer events arrive in pairs (4.6 / 0.6 ms
@@ -370,27 +374,28 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
         if (i >= 1 && ordered)
           for (int ci = 0; ci < ncs; ++ci)
             for (int cj = 0; cj < ncs; ++cj)
-              if (cj != ci && (e = cudaStreamWaitEvent(p->cs[ci], p->ev_copy[slot ^ 1][cj], 0)))
+              if (cj != ci && (e = cudaStreamWaitEvent(D.cs[ci], D.ev_copy[slot ^ 1][cj], 0)))
                 return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        if ((e = submit_copies(p, D, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
         for (int ci = 0; ci < ncs; ++ci)
-          if ((e = cudaStreamWaitEvent(s, p->ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+          if ((e = cudaStreamWaitEvent(s, D.ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = launch_group(0))) return cuda_fail(e, "scatter kernel launch");
-        if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
+        if ((e = cudaEventRecord(D.ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
       } else {
         // gathers into the slot (after its previous copies drained), then copies to the host tier
-        if (i >= 2)
+        if (seq >= 2)
           for (int ci = 0; ci < ncs; ++ci)
-            if ((e = cudaStreamWaitEvent(s, p->ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+            if ((e = cudaStreamWaitEvent(s, D.ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = launch_group(1))) return cuda_fail(e, "gather kernel launch");
-        if ((e = cudaEventRecord(p->ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
+        if ((e = cudaEventRecord(D.ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
         for (int ci = 0; ci < ncs; ++ci)
-          if ((e = cudaStreamWaitEvent(p->cs[ci], p->ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+          if ((e = cudaStreamWaitEvent(D.cs[ci], D.ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+        if ((e = submit_copies(p, D, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
       }
       p->counters.dma_copies += static_cast<int64_t>(dst.size());
       last_slot = slot;
       ++i;
+      ++seq;
     }
     if (dir == 0 && pieces.empty()) {
       for (int g = 0; g < gl; ++g)
@@ -398,16 +403,16 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     } else if (dir == 1) {
       // host bytes of the group are written once every copy stream has passed its last piece
       if (!pieces.empty())
-        for (int c = 1; c < p->ncs; ++c)
-          if ((e = cudaStreamWaitEvent(p->cs[0], p->ev_copy[last_slot][c], 0)))
+        for (int c = 1; c < D.ncs; ++c)
+          if ((e = cudaStreamWaitEvent(D.cs[0], D.ev_copy[last_slot][c], 0)))
             return cuda_fail(e, "cudaStreamWaitEvent");
       for (int g = 0; g < gl; ++g)
-        if ((e = cudaEventRecord(layer_event(lg + g), p->cs[0]))) return cuda_fail(e, "cudaEventRecord");
+        if ((e = cudaEventRecord(layer_event(lg + g), D.cs[0]))) return cuda_fail(e, "cudaEventRecord");
     }
   }
   if (dir == 1 && i > 0)  // join: the caller's stream is ordered after every copy
-    for (int ci = 0; ci < p->ncs; ++ci)
-      if ((e = cudaStreamWaitEvent(s, p->ev_copy[last_slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
+    for (int ci = 0; ci < D.ncs; ++ci)
+      if ((e = cudaStreamWaitEvent(s, D.ev_copy[last_slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
   return STRATA_OK;
 }
 

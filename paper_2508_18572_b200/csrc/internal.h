@@ -139,20 +139,27 @@ struct strata_pool {
   int32_t* err_host = nullptr;        // pinned
   int tma_smem = 0;
   strata_counters counters = {};
-  // STRATA_ENGINE_DMA: double-buffered HBM staging ring, copy streams and their events (lazy)
-  // capacity; `ncs` are used (env STRATA_COPY_STREAMS).  Default 1: with the per-piece barrier one
-  // in-order copy stream beats 2-8 streams on every config and in both directions
+  // STRATA_ENGINE_DMA, one state per direction (0 load, 1 offload; lazy): a double-buffered HBM
+  // staging ring, copy streams and their events.  Separate per direction so a load and an offload
+  // of one pool can be in flight at once on different streams (both directions of the link);
+  // `seq` numbers the pieces of a direction across operations, so an operation on another stream
+  // waits for the previous one's last use of a staging slot (tests/test_gpu_concurrent.py).
+  // Copy streams: capacity kCopyStreams, `ncs` used (env STRATA_COPY_STREAMS).  Default 1: one
+  // in-order copy stream beats 2-8 on every config and in both directions
   // (profiles/r01/copy_streams: Llama-8B 55.36 vs 54.37 GB/s at 1 vs 4; bidirectional 101 vs 91)
   static constexpr int kCopyStreams = 8;
-  int ncs = 1;
-  char* stage[2] = {nullptr, nullptr};
-  size_t stage_bytes = 0;             // bytes per staging slot
+  struct DmaDir {
+    int ncs = 1;
+    char* stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;           // bytes per staging slot
+    cudaStream_t cs[kCopyStreams] = {};
+    cudaEvent_t ev_fork = nullptr;
+    cudaEvent_t ev_slot[2] = {nullptr, nullptr};   // staging slot reusable
+    cudaEvent_t ev_copy[2][kCopyStreams] = {};     // a slot's copies done, per stream
+    uint64_t seq = 0;                 // pieces issued in this direction so far
+  } dma[2];
   int32_t* slot_ids = nullptr;        // device iota [0, slot_cap): chunk index of each staging slot
   int64_t slot_cap = 0;
-  cudaStream_t cs[kCopyStreams] = {};
-  cudaEvent_t ev_fork = nullptr;
-  cudaEvent_t ev_slot[2] = {nullptr, nullptr};                 // staging slot reusable
-  cudaEvent_t ev_copy[2][kCopyStreams] = {};                   // a slot's copies done, per stream
   // fused LDG operations (lazy): per op slot, L arrival counters + L layer flags (device), and a side
   // stream that turns each flag into the layer's event (cuStreamWaitValue32 + cudaEventRecord)
   uint32_t* fused_sync = nullptr;     // [kEventRing][2][L]

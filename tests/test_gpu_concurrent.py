@@ -50,10 +50,12 @@ def test_two_operations_in_flight(kinds, ea, eb):
         dev0k = [t.cpu().numpy() for t in k]
         dev0v = [t.cpu().numpy() for t in v]
         sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+        # the device index lists must outlive the operations (include/strata.h): keep both alive
+        reqs = [st.Requests.from_kvgen(qa), st.Requests.from_kvgen(qb)]
         torch.cuda.synchronize()
-        for kind, q, eng, s in ((kinds[0], qa, ea, sa), (kinds[1], qb, eb, sb)):
+        for kind, r, eng, s in ((kinds[0], reqs[0], ea, sa), (kinds[1], reqs[1], eb, sb)):
             op = pool.load if kind == "load" else pool.offload
-            op(st.Requests.from_kvgen(q), stream=s, engine=eng)
+            op(r, stream=s, engine=eng)
         torch.cuda.synchronize()
         # expected: apply both (disjoint) operations to the pre-states with the oracle
         ek, ev_ = [a.copy() for a in dev0k], [a.copy() for a in dev0v]
