@@ -251,6 +251,11 @@ class HostPool:
         if x is None:
             x = reqs._xcache[key] = reqs.xfer(key[0], key[1], engine, num_ctas, threads, layer_group=layer_group)
         check(fn(self._hptr, ctypes.byref(x), ctypes.c_void_p(_stream_handle(stream)), self._ticket), name)
+        if stream is not None and hasattr(stream, "cuda_stream"):
+            # the kernels read the device index lists on `stream`: keep torch's caching allocator
+            # from handing their memory out again before that stream passes this operation
+            reqs.host_chunks_d.record_stream(stream)
+            reqs.dev_pages_d.record_stream(stream)
         return self._ticket.value
 
     def load(self, reqs: Requests, layer_begin: int = 0, layer_end: Optional[int] = None, stream=None,
