@@ -49,6 +49,8 @@
  * independent.  Operations of one handle may be in flight at once on different streams (e.g. a
  * load and an offload: both directions of the link); the library orders their use of its internal
  * staging buffers, the caller keeps their destinations disjoint (tests/test_gpu_concurrent.py).
+ * Exception: a STRATA_ENGINE_DMA operation captured into a CUDA graph is ordered only by the graph;
+ * do not replay it while another DMA operation of the same pool and direction is in flight.
  */
 #ifndef STRATA_H
 #define STRATA_H

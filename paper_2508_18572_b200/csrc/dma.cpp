@@ -242,7 +242,12 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   bool strided = true;   // env STRATA_DMA_STRIDED=0: one copy per chunk (A/B only)
   if (const char* v = getenv("STRATA_DMA_STRIDED")) strided = atoi(v) != 0;
   int64_t i = 0;                 // pieces of this operation
-  uint64_t& seq = D.seq;          // pieces of this direction, across operations
+  // pieces of this direction, across operations; a graph capture starts its own sequence (its
+  // nodes may not depend on uncaptured work, and a replay is ordered by the graph's own edges)
+  cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+  if ((e = cudaStreamIsCapturing(s, &capst))) return cuda_fail(e, "cudaStreamIsCapturing");
+  uint64_t capture_seq = 0;
+  uint64_t& seq = capst == cudaStreamCaptureStatusActive ? capture_seq : D.seq;
   int last_slot = 0;
   auto layer_event = [&](int32_t l) { return p->events[size_t(slot_ev) * (L + 1) + 1 + l]; };
   for (int32_t lg = x->layer_begin; lg < x->layer_end; lg += G) {
