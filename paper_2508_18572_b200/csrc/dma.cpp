@@ -147,14 +147,19 @@ static cudaError_t submit_copies(strata_pool* p, strata_pool::DmaDir& D, std::ve
   return cudaSuccess;
 }
 
-int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata::XferParams xp, cudaStream_t s,
-                 int dir, int slot_ev) {
-  if (!x->host_chunks_host && plan.total_tokens > 0)
-    return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
-  const int64_t C = p->d.chunk_tokens, P = p->d.page_size, tok = p->tok_bytes;
-  const int L = p->d.num_layers;
-  // chunk positions of the call, request by request
-  std::vector<ChunkPos> pos;
+// Geometry of one DMA operation: what a chunk position contributes to the host <-> staging copies.
+struct DmaGeom {
+  int64_t C, P, tok, nkv, hb, Hl, h0;
+  size_t unit;    // one chunk-layer of this GPU's heads: nkv*C*H*D*e
+  int G;          // layers per copy run (layer group)
+  size_t gunit;   // staging bytes per chunk position: G*unit
+  bool hm;        // head-major host chunks (R28)
+  int64_t lay() const { return nkv * C * hb; }   // head-major: one layer of one head
+};
+
+// The call's chunk positions, request by request (a position = the tokens of one host chunk).
+static int collect_positions(const strata_pool* p, const strata_xfer* x, const Plan& plan, std::vector<ChunkPos>& pos) {
+  const int64_t C = p->d.chunk_tokens;
   for (int32_t r : plan.reqs) {
     const int64_t n = x->num_tokens[r];
     const int64_t oc = x->chunk_offset ? x->chunk_offset[r] : 0;
@@ -168,51 +173,181 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
       i += cnt;
     }
   }
-  const int64_t nkv = p->nkv;
-  const size_t unit = static_cast<size_t>(nkv * C * tok);           // one chunk-layer: K rows, V rows
+  return STRATA_OK;
+}
+
+// Pieces: <= cap chunk positions and <= kMaxReqsPerLaunch requests each.
+static std::vector<Piece> make_pieces(const std::vector<ChunkPos>& pos, size_t cap) {
+  std::vector<Piece> v;
+  for (size_t k = 0; k < pos.size();) {
+    Piece pc{k, 0};
+    int nreq = 0;
+    int32_t last = -1;
+    while (k < pos.size() && pc.count < cap) {
+      if (pos[k].req != last) {
+        if (nreq == kMaxReqsPerLaunch) break;
+        ++nreq;
+        last = pos[k].req;
+      }
+      ++pc.count;
+      ++k;
+    }
+    v.push_back(pc);
+  }
+  return v;
+}
+
+struct CopyList {
+  std::vector<void*> dst, src;
+  std::vector<size_t> sz;
+  std::vector<Copy2D> c2d;
+  void clear() {
+    dst.clear();
+    src.clear();
+    sz.clear();
+    c2d.clear();
+  }
+  void add(char* host, char* staged, int64_t bytes, int dir) {   // one run: host <-> staging
+    dst.push_back(dir == 0 ? staged : host);
+    src.push_back(dir == 0 ? host : staged);
+    sz.push_back(static_cast<size_t>(bytes));
+  }
+};
+
+// Host <-> staging copies of one piece for layers [lg, lg+gl): staging slot j holds chunk position
+// j's G layers in the host tier's own order for this GPU's heads — token-major [G][KV][C][H][D], or
+// head-major [H][G][KV][C][D] (R28).  Runs of full chunks with consecutive host ids become one
+// strided copy (per head for head-major); the rest is one copy per contiguous run.
+static void build_copies(strata_pool* p, const strata_xfer* x, const std::vector<ChunkPos>& pos, const Piece& pc,
+                         const DmaGeom& m, int32_t lg, int gl, char* stage, int dir, bool strided, CopyList& out) {
+  auto host_chunk = [&](size_t j) {
+    const ChunkPos& c = pos[pc.first + j];
+    return int64_t(x->host_chunks_host[x->chunk_start[c.req] + c.cq]);
+  };
+  auto full = [&](size_t j) { return pos[pc.first + j].lo == 0 && pos[pc.first + j].cnt == m.C; };
+  const int64_t lay = m.lay();
+  for (size_t j = 0; j < pc.count; ++j) {
+    const ChunkPos& cp = pos[pc.first + j];
+    const int64_t hc = host_chunk(j);
+    char* const hbase = p->host + hc * p->chunk_bytes;
+    char* const d = stage + j * m.gunit;
+    if (strided && full(j)) {   // full chunks: extend over consecutive host ids
+      size_t k = 1;
+      while (j + k < pc.count && full(j + k) && host_chunk(j + k) == hc + int64_t(k)) ++k;
+      if (k >= 2) {
+        // token-major: the group's layers of a chunk are one block; head-major: one block per head
+        // of this GPU (the layers of head h0+b, [L][KV][C][D] inside the chunk)
+        const int nblk = m.hm ? int(m.Hl) : 1;
+        for (int b = 0; b < nblk; ++b) {
+          char* h0p = hbase + (m.hm ? (m.h0 + b) * p->host_head_stride + int64_t(lg) * lay : int64_t(lg) * int64_t(m.unit));
+          char* d0p = d + (m.hm ? size_t(b) * m.G * lay : 0);
+          const size_t width = m.hm ? size_t(gl) * lay : size_t(gl) * m.unit;
+          if (dir == 0) out.c2d.push_back({d0p, m.gunit, h0p, size_t(p->chunk_bytes), width, k});
+          else out.c2d.push_back({h0p, size_t(p->chunk_bytes), d0p, m.gunit, width, k});
+          p->counters.dma_copies += 1;
+        }
+        j += k - 1;
+        continue;
+      }
+    }
+    if (m.hm) {
+      // head-major: head h0+hh of the chunk is a one-head page-first chunk [L][KV][C][D]
+      auto hoff = [&](int64_t hh, int g, int kv) {
+        return (m.h0 + hh) * p->host_head_stride + int64_t(lg + g) * lay + kv * m.C * m.hb;
+      };
+      auto soff = [&](int64_t hh, int g, int kv) { return (hh * m.G + g) * lay + kv * m.C * m.hb; };
+      for (int64_t hh = 0; hh < m.Hl; ++hh) {
+        if (full(j)) {
+          out.add(hbase + hoff(hh, 0, 0), d + soff(hh, 0, 0), gl * lay, dir);   // the group's layers of the head
+        } else {
+          for (int g = 0; g < gl; ++g)
+            for (int kv = 0; kv < m.nkv; ++kv)
+              out.add(hbase + hoff(hh, g, kv) + cp.lo * m.hb, d + soff(hh, g, kv) + cp.lo * m.hb, cp.cnt * m.hb, dir);
+        }
+      }
+    } else {
+      char* const h = hbase + int64_t(lg) * int64_t(m.unit);
+      if (full(j)) {
+        out.add(h, d, gl * int64_t(m.unit), dir);   // the group's K,V runs are adjacent: one copy
+      } else {
+        for (int g = 0; g < gl; ++g) {
+          const int64_t o = g * int64_t(m.unit);
+          out.add(h + o + cp.lo * m.tok, d + o + cp.lo * m.tok, cp.cnt * m.tok, dir);   // K rows of layer lg+g
+          if (m.nkv == 2)                                                                // V rows
+            out.add(h + o + (m.C + cp.lo) * m.tok, d + o + (m.C + cp.lo) * m.tok, cp.cnt * m.tok, dir);
+        }
+      }
+    }
+  }
+}
+
+// Request table of a piece: sub-requests whose "chunks" are staging slots 0..count-1.  Returns the
+// piece's token count.
+static int32_t piece_table(const strata_xfer* x, const std::vector<ChunkPos>& pos, const Piece& pc, int64_t P,
+                           strata::ReqTable& rt) {
+  rt.n = 0;
+  int32_t acc = 0;
+  for (size_t j = 0; j < pc.count; ++j) {
+    const ChunkPos& cp = pos[pc.first + j];
+    if (j == 0 || cp.req != pos[pc.first + j - 1].req) {
+      const int k = rt.n++;
+      const int64_t op = x->page_offset ? x->page_offset[cp.req] : 0;
+      const int64_t pi0 = op + cp.i0;
+      rt.tok_end[k] = acc;
+      rt.chunk_base[k] = static_cast<int32_t>(j);
+      rt.off_c[k] = cp.lo;
+      rt.page_base[k] = static_cast<int32_t>(x->page_start[cp.req] + pi0 / P);
+      rt.off_p[k] = static_cast<int32_t>(pi0 % P);
+    }
+    acc += cp.cnt;
+    rt.tok_end[rt.n - 1] = acc;
+  }
+  return acc;
+}
+
+int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata::XferParams xp, cudaStream_t s,
+                 int dir, int slot_ev) {
+  if (!x->host_chunks_host && plan.total_tokens > 0)
+    return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
+  const int L = p->d.num_layers;
+  std::vector<ChunkPos> pos;
+  int rc = collect_positions(p, x, plan, pos);
+  if (rc) return rc;
+  DmaGeom m;
+  m.C = p->d.chunk_tokens;
+  m.P = p->d.page_size;
+  m.tok = p->tok_bytes;
+  m.nkv = p->nkv;
+  m.hb = p->head_bytes;
+  m.Hl = p->d.num_heads;
+  m.h0 = p->head_begin;
+  m.hm = p->head_major;
+  m.unit = static_cast<size_t>(m.nkv * m.C * m.tok);
   // layers per copy run.  Loads keep per-layer granularity (grouping does not raise H2D throughput,
   // profiles/r01/sweep_groups*.jsonl); offloads ("backup", a non-critical path) group
   // layers until a run is >= 128 KiB, which D2H copies need (70B TP=8 rank: 44.6 -> 55.8 GB/s).
   int G = x->layer_group;
   if (G <= 0)
-    G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + int64_t(unit) - 1) / int64_t(unit)));
-  G = std::max(1, std::min(G, std::max(1, x->layer_end - x->layer_begin)));
-  const size_t gunit = unit * static_cast<size_t>(G);                 // staging bytes per chunk
+    G = dir == 0 ? 1 : static_cast<int>(std::min<int64_t>(8, (kDmaMinOffloadRun + int64_t(m.unit) - 1) / int64_t(m.unit)));
+  m.G = std::max(1, std::min(G, std::max(1, x->layer_end - x->layer_begin)));
+  m.gunit = m.unit * static_cast<size_t>(m.G);
   size_t stage_target = kStageTarget;
   if (const char* v = getenv("STRATA_STAGE_MB")) stage_target = std::max<size_t>(1, strtoull(v, nullptr, 10)) << 20;
-  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), stage_target / gunit));
+  const size_t per_piece = std::max<size_t>(1, std::min(pos.size(), stage_target / m.gunit));
   bool ordered = true;   // env STRATA_DMA_ORDERED=0 drops the piece barrier (A/B only)
   if (const char* v = getenv("STRATA_DMA_ORDERED")) ordered = atoi(v) != 0;
-  // pieces: <= cap chunk positions and <= kMaxReqsPerLaunch requests each
-  auto make_pieces = [&](size_t cap) {
-    std::vector<Piece> v;
-    for (size_t k = 0; k < pos.size();) {
-      Piece pc{k, 0};
-      int nreq = 0;
-      int32_t last = -1;
-      while (k < pos.size() && pc.count < cap) {
-        if (pos[k].req != last) {
-          if (nreq == kMaxReqsPerLaunch) break;
-          ++nreq;
-          last = pos[k].req;
-        }
-        ++pc.count;
-        ++k;
-      }
-      v.push_back(pc);
-    }
-    return v;
-  };
-  const std::vector<Piece> pieces = make_pieces(per_piece);
+  bool strided = true;   // env STRATA_DMA_STRIDED=0: one copy per chunk (A/B only)
+  if (const char* v = getenv("STRATA_DMA_STRIDED")) strided = atoi(v) != 0;
+  const std::vector<Piece> pieces = make_pieces(pos, per_piece);
   // The first and the last layer group are cut into `edge` times smaller pieces: the first layer's
   // event then waits for one small scatter instead of a whole-layer one (earlier start of layer-wise
   // prefill), and the op's tail, the last scatter with no copy left to hide it, shrinks the same way.
   int edge = 4;   // env STRATA_DMA_EDGE_SPLIT (1 = off)
   if (const char* v = getenv("STRATA_DMA_EDGE_SPLIT")) edge = std::max(1, atoi(v));
-  const size_t edge_cap = std::min(per_piece, std::max<size_t>({1, per_piece / size_t(edge), kDmaMinEdgePiece / gunit}));
-  const std::vector<Piece> edge_pieces = edge_cap < per_piece ? make_pieces(edge_cap) : pieces;
+  const size_t edge_cap = std::min(per_piece, std::max<size_t>({1, per_piece / size_t(edge), kDmaMinEdgePiece / m.gunit}));
+  const std::vector<Piece> edge_pieces = edge_cap < per_piece ? make_pieces(pos, edge_cap) : pieces;
   strata_pool::DmaDir& D = p->dma[dir];
-  int rc = ensure_dma(p, D, per_piece * gunit, static_cast<int64_t>(per_piece));
+  rc = ensure_dma(p, D, per_piece * m.gunit, static_cast<int64_t>(per_piece));
   if (rc) return rc;
 
   cudaError_t e;
@@ -220,27 +355,18 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;
   xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows
   const int ctas = x->num_ctas ? x->num_ctas : kDefaultCtasScatter;
-  // staging slot j holds chunk position j's G layers: [G][K,V][C][H][D], a compact host tier
-  xp.chunk_bytes = static_cast<int64_t>(gunit);
-  xp.kv_off = C * tok;
+  // the scatter / gather kernel sees the staging slots as a compact host tier (chunk = slot)
+  xp.chunk_bytes = static_cast<int64_t>(m.gunit);
+  xp.kv_off = m.hm ? m.C * m.hb : m.C * m.tok;
   xp.host_chunks = p->slot_ids;
-  // staging keeps the host tier's order for this GPU's heads only: token-major [G][KV][C][H][D], or
-  // head-major [H][G][KV][C][D] (R28)
-  const bool hm = p->head_major;
-  const int64_t hb = p->head_bytes, Hl = p->d.num_heads, h0 = p->head_begin;
-  if (hm) xp.kv_off = C * hb;
-  xp.host_tok_stride = hm ? hb : tok;
+  xp.host_tok_stride = m.hm ? m.hb : m.tok;
   xp.host_head_off = 0;
-  xp.host_head_stride = hm ? int64_t(G) * nkv * C * hb : hb;
+  xp.host_head_stride = m.hm ? int64_t(m.G) * m.lay() : m.hb;
 
   if ((e = cudaEventRecord(D.ev_fork, s))) return cuda_fail(e, "cudaEventRecord");
   for (int ci = 0; ci < D.ncs; ++ci)
     if ((e = cudaStreamWaitEvent(D.cs[ci], D.ev_fork, 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-  std::vector<void*> dst, src;
-  std::vector<size_t> sz;
-  std::vector<Copy2D> c2d;
-  bool strided = true;   // env STRATA_DMA_STRIDED=0: one copy per chunk (A/B only)
-  if (const char* v = getenv("STRATA_DMA_STRIDED")) strided = atoi(v) != 0;
+  CopyList cl;
   int64_t i = 0;                 // pieces of this operation
   // pieces of this direction, across operations; a graph capture starts its own sequence (its
   // nodes may not depend on uncaptured work, and a replay is ordered by the graph's own edges)
@@ -250,114 +376,25 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   uint64_t& seq = capst == cudaStreamCaptureStatusActive ? capture_seq : D.seq;
   int last_slot = 0;
   auto layer_event = [&](int32_t l) { return p->events[size_t(slot_ev) * (L + 1) + 1 + l]; };
-  for (int32_t lg = x->layer_begin; lg < x->layer_end; lg += G) {
-    const int gl = std::min<int>(G, x->layer_end - lg);   // layers in this group
-    const std::vector<Piece>& gp = (lg == x->layer_begin || lg + G >= x->layer_end) ? edge_pieces : pieces;
+  for (int32_t lg = x->layer_begin; lg < x->layer_end; lg += m.G) {
+    const int gl = std::min<int>(m.G, x->layer_end - lg);   // layers in this group
+    const std::vector<Piece>& gp = (lg == x->layer_begin || lg + m.G >= x->layer_end) ? edge_pieces : pieces;
     for (const Piece& pc : gp) {
       const bool last_piece = &pc == &gp.back();
       const int slot = static_cast<int>(seq & 1);
       char* stage = D.stage[slot];
-      // copy list of this piece for layers [lg, lg+gl) (host <-> staging slot)
-      dst.clear();
-      src.clear();
-      sz.clear();
-      c2d.clear();
-      auto host_chunk = [&](size_t j) {
-        const ChunkPos& c = pos[pc.first + j];
-        return int64_t(x->host_chunks_host[x->chunk_start[c.req] + c.cq]);
-      };
-      auto full = [&](size_t j) { return pos[pc.first + j].lo == 0 && pos[pc.first + j].cnt == C; };
-      for (size_t j = 0; j < pc.count; ++j) {
-        const ChunkPos& cp = pos[pc.first + j];
-        const int64_t hc = host_chunk(j);
-        if (strided && full(j)) {   // full chunks: extend over consecutive host ids
-          size_t k = 1;
-          while (j + k < pc.count && full(j + k) && host_chunk(j + k) == hc + int64_t(k)) ++k;
-          if (k >= 2) {
-            // token-major: the group's layers of a chunk are one block; head-major: one block per
-            // head of this GPU (the layers of head h0+hh, [L][KV][C][D] inside the chunk)
-            const int64_t lay = nkv * C * hb;
-            const int nblk = hm ? int(Hl) : 1;
-            for (int b = 0; b < nblk; ++b) {
-              char* h0p = p->host + hc * p->chunk_bytes +
-                          (hm ? (h0 + b) * p->host_head_stride + int64_t(lg) * lay : int64_t(lg) * int64_t(unit));
-              char* d0p = stage + j * gunit + (hm ? size_t(b) * G * lay : 0);
-              const size_t width = hm ? size_t(gl) * lay : size_t(gl) * unit;
-              if (dir == 0) c2d.push_back({d0p, gunit, h0p, size_t(p->chunk_bytes), width, k});
-              else c2d.push_back({h0p, size_t(p->chunk_bytes), d0p, gunit, width, k});
-              p->counters.dma_copies += 1;
-            }
-            j += k - 1;
-            continue;
-          }
-        }
-        char* h = p->host + hc * p->chunk_bytes + int64_t(lg) * int64_t(unit);
-        char* d = stage + j * gunit;
-        auto add = [&](int64_t off, int64_t bytes) {
-          dst.push_back(dir == 0 ? d + off : h + off);
-          src.push_back(dir == 0 ? h + off : d + off);
-          sz.push_back(static_cast<size_t>(bytes));
-        };
-        if (hm) {
-          // head-major: head h0+hh of the chunk is a one-head page-first chunk [L][KV][C][D]
-          const int64_t lay = nkv * C * hb;   // one layer of one head
-          auto hoff = [&](int64_t hh, int g, int kv) {
-            return (h0 + hh) * p->host_head_stride + int64_t(lg + g) * lay + kv * C * hb;
-          };
-          auto soff = [&](int64_t hh, int g, int kv) { return (hh * G + g) * lay + kv * C * hb; };
-          char* const hbase = p->host + hc * p->chunk_bytes;
-          auto addh = [&](int64_t hofs, int64_t sofs, int64_t bytes) {
-            dst.push_back(dir == 0 ? d + sofs : hbase + hofs);
-            src.push_back(dir == 0 ? hbase + hofs : d + sofs);
-            sz.push_back(static_cast<size_t>(bytes));
-          };
-          for (int64_t hh = 0; hh < Hl; ++hh) {
-            if (cp.lo == 0 && cp.cnt == C) {
-              addh(hoff(hh, 0, 0), soff(hh, 0, 0), gl * lay);          // the group's layers: one run per head
-            } else {
-              for (int g = 0; g < gl; ++g)
-                for (int kv = 0; kv < nkv; ++kv)
-                  addh(hoff(hh, g, kv) + cp.lo * hb, soff(hh, g, kv) + cp.lo * hb, cp.cnt * hb);
-            }
-          }
-        } else if (cp.lo == 0 && cp.cnt == C) {
-          add(0, gl * int64_t(unit));                  // the group's K,V runs are adjacent: one copy
-        } else {
-          for (int g = 0; g < gl; ++g) {
-            add(g * int64_t(unit) + cp.lo * tok, cp.cnt * tok);                     // K rows of layer lg+g
-            if (nkv == 2) add(g * int64_t(unit) + (C + cp.lo) * tok, cp.cnt * tok);  // V rows
-          }
-        }
-      }
-      // request table of the piece: sub-requests addressing staging slots
-      strata::ReqTable& rt = xp.rt;
-      rt.n = 0;
-      int32_t acc = 0;
-      for (size_t j = 0; j < pc.count; ++j) {
-        const ChunkPos& cp = pos[pc.first + j];
-        if (j == 0 || cp.req != pos[pc.first + j - 1].req) {
-          const int k = rt.n++;
-          const int64_t op = x->page_offset ? x->page_offset[cp.req] : 0;
-          const int64_t pi0 = op + cp.i0;
-          rt.tok_end[k] = acc;
-          rt.chunk_base[k] = static_cast<int32_t>(j);
-          rt.off_c[k] = cp.lo;
-          rt.page_base[k] = static_cast<int32_t>(x->page_start[cp.req] + pi0 / P);
-          rt.off_p[k] = static_cast<int32_t>(pi0 % P);
-        }
-        acc += cp.cnt;
-        rt.tok_end[rt.n - 1] = acc;
-      }
-      xp.ntok = acc;
+      cl.clear();
+      build_copies(p, x, pos, pc, m, lg, gl, stage, dir, strided, cl);
+      xp.ntok = piece_table(x, pos, pc, m.P, xp.rt);
       xp.host = stage;
-      const int64_t groups = (nkv * acc + xp.rows_per_group - 1) / xp.rows_per_group;
+      const int64_t groups = (m.nkv * xp.ntok + xp.rows_per_group - 1) / xp.rows_per_group;
       const int c = static_cast<int>(std::min<int64_t>(ctas, (groups * 32 + threads - 1) / threads));
       // one scatter / gather launch per layer of the group over the slot's layer sub-blocks
       auto launch_group = [&](int kdir) -> cudaError_t {
         for (int g = 0; g < gl; ++g) {
           xp.kbase = static_cast<char*>(p->k[lg + g]);
           xp.vbase = static_cast<char*>(p->v[lg + g]);
-          xp.layer_off = hm ? int64_t(g) * nkv * C * hb : int64_t(g) * int64_t(unit);
+          xp.layer_off = m.hm ? int64_t(g) * m.lay() : int64_t(g) * int64_t(m.unit);
           cudaError_t le = strata::launch_ldg(xp, kdir, c, threads, unroll, s);
           if (le != cudaSuccess) return le;
           ++p->counters.kernel_launches;
@@ -381,7 +418,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
             for (int cj = 0; cj < ncs; ++cj)
               if (cj != ci && (e = cudaStreamWaitEvent(D.cs[ci], D.ev_copy[slot ^ 1][cj], 0)))
                 return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, D, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        if ((e = submit_copies(p, D, cl.dst, cl.src, cl.sz, cl.c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
         for (int ci = 0; ci < ncs; ++ci)
           if ((e = cudaStreamWaitEvent(s, D.ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = launch_group(0))) return cuda_fail(e, "scatter kernel launch");
@@ -395,9 +432,9 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
         if ((e = cudaEventRecord(D.ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
         for (int ci = 0; ci < ncs; ++ci)
           if ((e = cudaStreamWaitEvent(D.cs[ci], D.ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, D, dst, src, sz, c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        if ((e = submit_copies(p, D, cl.dst, cl.src, cl.sz, cl.c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
       }
-      p->counters.dma_copies += static_cast<int64_t>(dst.size());
+      p->counters.dma_copies += static_cast<int64_t>(cl.dst.size());
       last_slot = slot;
       ++i;
       ++seq;
