@@ -128,9 +128,15 @@ static cudaError_t submit_copies(strata_pool* p, strata_pool::DmaDir& D, std::ve
     cudaError_t e = cudaMemcpy2DAsync(r.dst, r.dpitch, r.src, r.spitch, r.width, r.height, kind, D.cs[0]);
     if (e != cudaSuccess) return e;
   }
+  // env STRATA_DMA_NO_BATCH=1: plain cudaMemcpyAsync per run (A/B and tools that do not model the
+  // batch API, e.g. compute-sanitizer initcheck)
+  static const bool no_batch = [] {
+    const char* v = getenv("STRATA_DMA_NO_BATCH");
+    return v && atoi(v) != 0;
+  }();
   for (int c = 0; c < ns; ++c) {
     const size_t lo = n * c / ns, hi = n * (c + 1) / ns;
-    if (hi > lo && cap == cudaStreamCaptureStatusActive) {
+    if (hi > lo && (cap == cudaStreamCaptureStatusActive || no_batch)) {
       for (size_t i = lo; i < hi; ++i) {
         cudaError_t e = cudaMemcpyAsync(dst[i], src[i], sz[i], kind, D.cs[c]);
         if (e != cudaSuccess) return e;

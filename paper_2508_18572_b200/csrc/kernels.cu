@@ -427,9 +427,12 @@ __global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
+  // Every producer lane arrives on `full` itself, so each lane's address-table write is released by
+  // its own arrive (with one arrive by lane 0 after __syncwarp, compute-sanitizer racecheck reported
+  // the table writes as racing with the consumers' reads); consumers arrive once per warp.
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 32);
       mbar_init(&empty[s], kWsConsumers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -464,8 +467,9 @@ __global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel
       const unsigned later = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
       const int run = (later ? __ffs(later) - 1 : nvalid) - lane;
       tab_addr[s * 32 + lane] = reinterpret_cast<uint64_t>(dp);
-      __syncwarp();
+      // lane 0 also announces the stage's bytes; the phase cannot complete before its arrive
       if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nvalid * tok));
+      else mbar_arrive(&full[s]);
       __syncwarp();
       if (head) bulk_g2s(buf + static_cast<size_t>(s) * SB + lane * tok, hp, static_cast<uint32_t>(run * tok),
                          &full[s]);
