@@ -210,15 +210,16 @@ def test_dma_engine_piece_schedule(direction, edge, ordered, streams, monkeypatc
         c.close()
 
 
+@pytest.mark.parametrize("kv", [2, 1])
 @pytest.mark.parametrize("strided", ["1", "0"])
 @pytest.mark.parametrize("group", [1, 3])
 @pytest.mark.parametrize("direction", ["load", "offload"])
-def test_dma_strided_chunk_runs(direction, group, strided, monkeypatch):
+def test_dma_strided_chunk_runs(direction, group, strided, kv, monkeypatch):
     """Consecutive host chunk ids become one strided copy per run (cudaMemcpy2DAsync): requests
     with partial first / last chunks, runs broken by the request boundary and by a permuted tail,
     layer groups; the result stays the oracle's."""
     monkeypatch.setenv("STRATA_DMA_STRIDED", strided)
-    g = Geometry(5, 8, 128, 2, 1, 64, 40960, 700)
+    g = Geometry(5, 8, 128, 2, 1, 64, 40960, 700, kv=kv)
     rng = kvgen.rng_for(23)
     q = kvgen.make_requests(rng, [20000, 9000, 130], g.P, g.C, g.num_pages, g.num_chunks, offsets=True,
                             chunk_frag="identity")
