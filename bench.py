@@ -279,27 +279,42 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    barrier()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    c0 = pool.counters()
-    with ClockSampler(local) as clocks:
-        start.record(io)
-        last = None
-        host_s = 0.0   # CPU time inside the strata_load calls (submission only; they never block)
-        for i in range(args.steps):
-            marks[i].record(io)
-            h0 = time.perf_counter()
-            last = step()
-            host_s += time.perf_counter() - h0
-        marks[-1].record(io)
-        end.record(io)
+    def timed_region():
         barrier()
-    c1 = pool.counters()
-    launches = c1["kernel_launches"] - c0["kernel_launches"]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        c0 = pool.counters()
+        with ClockSampler(local) as clocks:
+            start.record(io)
+            last = None
+            host_s = 0.0   # CPU time inside the strata_load calls (submission; blocks only when queued ahead)
+            for i in range(args.steps):
+                marks[i].record(io)
+                h0 = time.perf_counter()
+                last = step()
+                host_s += time.perf_counter() - h0
+            marks[-1].record(io)
+            end.record(io)
+            barrier()
+        c1 = pool.counters()
+        step_ms = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps))
+        return (start.elapsed_time(end) / 1e3, step_ms, host_s, last, clocks,
+                c1["kernel_launches"] - c0["kernel_launches"], c1)
+
+    elapsed, step_ms, host_s, last, clocks, launches, c1 = timed_region()
+    # A timed region whose steps vary by more than 5 % (CV) saw something outside this process —
+    # e.g. the host still reclaiming memory a previous job freed, which slows the link itself — and is
+    # re-measured once; the first measurement is kept in the line.
+    cv = statistics.pstdev(step_ms) / statistics.mean(step_ms)
+    tcv = torch.tensor([cv], dtype=torch.float64, device=red_dev)
+    if world > 1:
+        dist.all_reduce(tcv, op=dist.ReduceOp.MAX)
+    remeasured = None
+    if float(tcv.item()) > 0.05:
+        remeasured = {"first_elapsed_s": round(elapsed, 4), "first_cv_max_over_ranks": round(float(tcv.item()), 4)}
+        time.sleep(2.0)
+        elapsed, step_ms, host_s, last, clocks, launches, c1 = timed_region()
     engine_used = ENGINE_NAMES.get(c1["last_engine"], str(c1["last_engine"]))
-    elapsed = start.elapsed_time(end) / 1e3
-    step_ms = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps))
     step_stats = {"median_ms": round(statistics.median(step_ms), 3),
                   "p10_ms": round(step_ms[int(0.1 * (len(step_ms) - 1))], 3),
                   "p90_ms": round(step_ms[int(0.9 * (len(step_ms) - 1))], 3),
@@ -428,6 +443,7 @@ def main():
             "zero_copy_kernels": zc,
             "per_layer_ms_last_step": [round(x, 4) for x in launch_ms],
             "host_submit_ms_per_step": round(host_s / args.steps * 1e3, 3),
+            "remeasured": remeasured,
         }
         print(json.dumps(out), flush=True)
     pool.close()
