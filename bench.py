@@ -90,7 +90,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,pcie.link.gen.current,pcie.link.width.current")
 
     def __init__(self, index: int):
         self.index = index
@@ -122,12 +122,14 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, reasons, links = [], [], set(), set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
+            if len(f) >= 9:
+                links.add(f"gen{f[7]} x{f[8]}")   # the host link the transfers use (PCIe state)
             try:
                 sm.append(float(f[0]))
                 mx.append(float(f[1]))
@@ -139,7 +141,7 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "pcie_link": sorted(links)}
 
 
 def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 10.0):
