@@ -45,6 +45,25 @@ def test_deepseek_latent_small(engine, P):
         c.close()
 
 
+@pytest.mark.parametrize("engine", ENGINES)
+def test_deepseek_fp8_latent_rows(engine):
+    """FP8 MLA cache rows as FlashMLA stores them: 512 fp8 latent + 4 fp32 scales + 64 bf16 rope
+    = 656 B per token and layer (41 vectors: neither a power of two nor a multiple of 32)."""
+    g = _g(L=2, H=1, D=656, P=64, C=64, num_pages=40, num_chunks=40, e=1)
+    q = kvgen.make_requests(kvgen.rng_for(47), [1500, 301], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
+    c = GpuCase(g, q, seed=9)
+    try:
+        c.pool.load(c.reqs, engine=engine)
+        torch.cuda.synchronize()
+        c.check_load(0, g.L)
+        before = c.pool.host.copy()
+        c.pool.offload(c.reqs, engine=engine)
+        torch.cuda.synchronize()
+        assert np.array_equal(c.pool.host, c.expected_offload(before, 0, g.L))
+    finally:
+        c.close()
+
+
 @pytest.mark.parametrize("i", range(60))
 def test_fuzz_single_kv(i):
     rng = kvgen.rng_for(5000 + i)
