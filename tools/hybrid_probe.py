@@ -18,7 +18,11 @@ import paper_2508_18572_b200 as st  # noqa: E402
 
 def main():
     g = kvgen.geometry("llama8b_32k")
-    comp, sa, sb = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    hi = "--high-priority-io" in sys.argv        # I/O streams at the highest priority
+    lo_p, hi_p = torch.cuda.Stream.priority_range()
+    comp = torch.cuda.Stream()
+    sa, sb = (torch.cuda.Stream(priority=hi_p), torch.cuda.Stream(priority=hi_p)) if hi else \
+        (torch.cuda.Stream(), torch.cuda.Stream())
     kv = [torch.randn(16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda") for _ in range(32)]
 
     def decode():
@@ -44,7 +48,7 @@ def main():
         return statistics.median(a.elapsed_time(b) for a, b in evs)
 
     alone = t_decode()
-    for f in (0.0, 0.1, 0.2, 0.3, 1.0):
+    for f in ((0.0, 1.0) if hi else (0.0, 0.1, 0.2, 0.3, 1.0)):
         n_ldg = int(round(32768 * (1 - f) / 64)) * 64
         n_ce = 32768 - n_ldg
         q = kvgen.make_requests(kvgen.rng_for(1), [max(n_ldg, 64)], g.P, g.C, g.num_pages, g.num_chunks)
@@ -84,7 +88,7 @@ def main():
             one()
         co = t_decode()
         torch.cuda.synchronize()
-        print(json.dumps({"ce_fraction": round(n_ce / 32768, 3), "load_gbs": round(gbs, 2),
+        print(json.dumps({"ce_fraction": round(n_ce / 32768, 3), "io_high_priority": hi, "load_gbs": round(gbs, 2),
                           "decode_alone_ms": round(alone, 4), "decode_corun_ms": round(co, 4),
                           "decode_slowdown": round(co / alone - 1, 4)}), flush=True)
         pool.close()

@@ -22,6 +22,7 @@ import os
 import statistics
 import sys
 import threading
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -54,7 +55,27 @@ def make_decode():
     return run
 
 
+CLOCKS = []   # (sm MHz, power W) samples of the last time_proxy block
+
+
+def _sample_clocks(stop):
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        while not stop[0]:
+            CLOCKS.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                           pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0))
+            time.sleep(0.002)
+    except Exception:
+        pass
+
+
 def time_proxy(fn, stream, reps):
+    CLOCKS.clear()
+    stop = [False]
+    th = threading.Thread(target=_sample_clocks, args=(stop,), daemon=True)
+    th.start()
     evs = []
     with torch.cuda.stream(stream):
         fn()
@@ -65,7 +86,15 @@ def time_proxy(fn, stream, reps):
             b.record(stream)
             evs.append((a, b))
     torch.cuda.synchronize()
+    stop[0] = True
+    th.join()
     return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+
+def clock_summary():
+    if not CLOCKS:
+        return None
+    return {"sm_mhz": statistics.median(c for c, _ in CLOCKS), "power_w": round(statistics.median(p for _, p in CLOCKS), 1)}
 
 
 def main():
@@ -137,21 +166,35 @@ def main():
             b.synchronize()
             io_alone = 3 * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
             for name, fn in proxies.items():
-                # keep the I/O stream busy for the whole proxy measurement
-                n_loads = max(2, int(alone[name] * args.reps / (bytes_load / io_alone / 1e6)) + 2)
-                torch.cuda.synchronize()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(io)
-                for _ in range(n_loads):
-                    load()
-                b.record(io)
-                t_co = time_proxy(fn, comp, args.reps)
-                b.synchronize()
-                io_co = n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
-                print(json.dumps({"kind": "corun", "graph": args.graph, "engine": eng, "ctas": c, "layer_group": G, "proxy": name,
-                                  "proxy_alone_ms": round(alone[name], 4), "proxy_corun_ms": round(t_co, 4),
-                                  "slowdown": round(t_co / alone[name] - 1, 4), "io_alone_gbs": round(io_alone, 2),
-                                  "io_corun_gbs_upper": round(io_co, 2)}), flush=True)
+                # Alone and co-run measurements alternate (3 rounds, medians): a baseline taken once at
+                # the start read up to 13 % slow for the decode proxy (after the GEMM proxy), and two
+                # back-to-back GEMM blocks drift with power state, so each co-run gets its own
+                # neighbouring alone measurement.
+                alone_ms, co_ms, io_cos, clk = [], [], [], []
+                for _r in range(3):
+                    torch.cuda.synchronize()
+                    alone_ms.append(time_proxy(fn, comp, args.reps))
+                    clk.append(("alone", clock_summary()))
+                    # keep the I/O stream busy for the whole proxy measurement
+                    n_loads = max(2, int(alone_ms[-1] * args.reps / (bytes_load / io_alone / 1e6)) + 2)
+                    torch.cuda.synchronize()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(io)
+                    for _ in range(n_loads):
+                        load()
+                    b.record(io)
+                    co_ms.append(time_proxy(fn, comp, args.reps))
+                    clk.append(("corun", clock_summary()))
+                    b.synchronize()
+                    io_cos.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
+                al, co = statistics.median(alone_ms), statistics.median(co_ms)
+                print(json.dumps({"kind": "corun", "graph": args.graph, "engine": eng, "ctas": c, "layer_group": G,
+                                  "proxy": name, "proxy_alone_ms": round(al, 4), "proxy_corun_ms": round(co, 4),
+                                  "slowdown": round(co / al - 1, 4),
+                                  "slowdown_rounds": [round(x / y - 1, 4) for x, y in zip(co_ms, alone_ms)],
+                                  "io_alone_gbs": round(io_alone, 2),
+                                  "io_corun_gbs_upper": round(statistics.median(io_cos), 2),
+                                  "clocks": clk}), flush=True)
     pool.close()
 
 
