@@ -104,6 +104,8 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--groups", default="0", help="DMA layer_group values (engine 4 only)")
     ap.add_argument("--memcpy", type=int, default=0, help="also co-run a contiguous cudaMemcpyAsync loop (-1 engine)")
+    ap.add_argument("--cooldown", type=float, default=1.0,
+                    help="idle seconds before every alone / co-run block (power-state reset for the GEMM proxy)")
     ap.add_argument("--graph", type=int, default=0,
                     help="replay each proxy from a CUDA graph (as serving engines run decode): copy-engine "
                          "traffic delays the per-kernel launch fetches of eager proxies (ce_interference.py)")
@@ -173,11 +175,13 @@ def main():
                 alone_ms, co_ms, io_cos, clk = [], [], [], []
                 for _r in range(3):
                     torch.cuda.synchronize()
+                    time.sleep(args.cooldown)
                     alone_ms.append(time_proxy(fn, comp, args.reps))
                     clk.append(("alone", clock_summary()))
                     # keep the I/O stream busy for the whole proxy measurement
                     n_loads = max(2, int(alone_ms[-1] * args.reps / (bytes_load / io_alone / 1e6)) + 2)
                     torch.cuda.synchronize()
+                    time.sleep(args.cooldown)
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record(io)
                     for _ in range(n_loads):
