@@ -69,13 +69,13 @@ def main():
                                 chunk_frag=args.chunk_frag)
         nb = g.num_pages * g.P * g.token_bytes
         k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
-        v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+        v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)] if g.kv == 2 else None
         pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P,
                            chunk_tokens=g.C, k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks,
-                           flags=args.flags)
+                           flags=args.flags, host_heads=g.Ht, head_begin=g.h0, head_major=g.head_major)
         kvgen.fill_random(pool.host, 3)
         reqs = st.Requests.from_kvgen(q)
-        nbytes = 2 * g.L * q.total_tokens * g.token_bytes
+        nbytes = g.kv * g.L * q.total_tokens * g.token_bytes
         base = {"config": args.config, "P": P, "L": g.L, "tokens": q.total_tokens, "bytes": nbytes, "frag": args.frag,
                 "chunk_frag": args.chunk_frag, "flags": args.flags, "tag": args.tag,
                 "host_tier_bytes": g.host_bytes}
