@@ -140,7 +140,8 @@ typedef struct {
   int32_t layer_begin;            /* l0, half-open layer range [l0, l1) (R11) */
   int32_t layer_end;              /* l1, 0 <= l0 <= l1 <= L */
   int32_t engine;                 /* strata_engine */
-  int32_t num_ctas;               /* SM quota; 0 = library default */
+  int32_t num_ctas;               /* SM quota; 0 = library default (LDG: 2 CTAs
+                                     for loads, 1 for offloads — the paper's quotas) */
   int32_t threads;                /* threads per CTA for STRATA_ENGINE_LDG; 0 = default */
   const int64_t* num_tokens;      /* [R] host: tokens to move per request (>= 0) */
   const int32_t* host_chunks;     /* device int32: all requests' chunk lists concatenated */

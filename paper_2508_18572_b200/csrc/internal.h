@@ -206,6 +206,10 @@ struct Plan {
 // The paper's quota: 2 CTAs x 1024 threads.  On B200 that moves 50.3 GB/s (90.7 % of
 // the link) with 0.8 % prefill-GEMM and 10.8 % decode slowdown (profiles/r01/interference2.jsonl).
 constexpr int kDefaultCtasLdg = 2;
+// The paper's backup quota: "one block for backing up data from GPU to CPU (a non-critical path),
+// where the bandwidth is already sufficient and overhead must be minimized".  On B200
+// one 1024-thread CTA offloads 39-40 GB/s and costs a co-running decode ~5 % instead of ~12 %.
+constexpr int kDefaultCtasLdgOffload = 1;
 constexpr int kDefaultThreadsLdg = 1024;   // host-read throughput of an SM scales with its warps
 constexpr int64_t kDmaMinLayerBytes = int64_t(4) << 20;
 constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;

@@ -336,7 +336,9 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;   // U=8 is compiled for <= 512 threads
   xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows (amortised index math)
-  int ctas = x->num_ctas ? x->num_ctas : (engine == STRATA_ENGINE_LDG ? kDefaultCtasLdg : kDefaultCtasTma);
+  int ctas = x->num_ctas ? x->num_ctas
+                         : engine == STRATA_ENGINE_LDG ? (dir == 0 ? kDefaultCtasLdg : kDefaultCtasLdgOffload)
+                                                       : kDefaultCtasTma;
   // small token rows shrink a TMA stage (<= 32 rows); keep ~64 KiB per stage-CTA in flight by
   // spreading over more CTAs (70B TP=8: 256 B rows -> 8 KiB stages -> 16 CTAs)
   if (!x->num_ctas && engine != STRATA_ENGINE_LDG && xp.tma_stage_bytes > 0)
