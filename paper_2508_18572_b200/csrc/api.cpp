@@ -357,8 +357,15 @@ int strata_wait_layer(strata_pool_t p, uint64_t ticket, int32_t layer, strata_st
   int slot = 0;
   int rc = find_op(p, ticket, layer, slot);
   if (rc) return rc;
-  cudaError_t e = cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(consumer),
-                                      p->events[size_t(slot) * (p->d.num_layers + 1) + 1 + layer], 0);
+  cudaError_t e;
+  // a fused operation's layers (except the last, whose event the caller's stream records) are
+  // waited on at their device flag directly, without the side stream's event hop
+  if (p->ops[slot].fused && layer + 1 < p->ops[slot].l1) {
+    e = strata::wait_fused_layer(p, slot, layer, reinterpret_cast<cudaStream_t>(consumer));
+    return e == cudaSuccess ? STRATA_OK : cuda_fail(e, "cuStreamWaitValue32");
+  }
+  e = cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(consumer),
+                          p->events[size_t(slot) * (p->d.num_layers + 1) + 1 + layer], 0);
   return e == cudaSuccess ? STRATA_OK : cuda_fail(e, "cudaStreamWaitEvent");
 }
 

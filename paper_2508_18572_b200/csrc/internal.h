@@ -129,7 +129,8 @@ struct strata_pool {
   size_t map_bytes = 0;               // mmap length
   // per-layer completion events: ring of kEventRing operations x L layers
   std::vector<cudaEvent_t> events;
-  struct Op { uint64_t ticket; int32_t l0, l1; };
+  // fused: the op ran as one fused LDG launch; its layer l is complete once flags[slot][l] >= epoch
+  struct Op { uint64_t ticket; int32_t l0, l1; bool fused = false; };
   Op ops[strata::kEventRing];
   uint64_t next_ticket = 1;
   // validate scratch (device)
@@ -227,6 +228,8 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, XferPar
                  int dir, int slot_ev);                                                       // dma.cpp
 void free_dma(strata_pool* p);
 void free_fused(strata_pool* p);
-bool ensure_fused(strata_pool* p);   // fused-LDG resources; false: unavailable (per-layer path) transfer.cpp                                                              // transfer.cpp                                                                // dma.cpp
+bool ensure_fused(strata_pool* p);   // fused-LDG resources; false: unavailable (per-layer path) transfer.cpp
+// Consumer-side wait on a fused operation's layer flag (stream memory op), transfer.cpp.
+cudaError_t wait_fused_layer(strata_pool* p, int slot, int32_t layer, cudaStream_t consumer);                                                              // transfer.cpp                                                                // dma.cpp
 
 }  // namespace strata

@@ -73,6 +73,14 @@ bool ensure_fused(strata_pool* p) {
   return true;
 }
 
+cudaError_t wait_fused_layer(strata_pool* p, int slot, int32_t layer, cudaStream_t consumer) {
+  const int L = p->d.num_layers;
+  uint32_t* flag = p->fused_sync + size_t(slot) * 2 * L + L + layer;
+  const uint32_t epoch = static_cast<uint32_t>(p->ops[slot].ticket);
+  return g_wait_value32(reinterpret_cast<CUstream>(consumer), reinterpret_cast<CUdeviceptr>(flag), epoch,
+                        CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
+
 void free_fused(strata_pool* p) {
   for (int i = 0; i < kEventRing; ++i)
     if (p->side[i]) {
@@ -386,6 +394,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     }
     e = strata::launch_ldg_fused(fp, dir, c, threads, s);
     if (e != cudaSuccess) return op_fail(e, "fused transfer kernel launch");
+    p->ops[slot].fused = true;
     ++p->counters.kernel_launches;
     cudaStream_t side = p->side[slot];
     // the last layer completes with the kernel: its event goes on the caller's stream, sparing the
