@@ -37,6 +37,8 @@
  *       device: pi = page_offset[r]  + i, page  dev_pages [page_start[r]  + pi / P], offset   pi % P
  *
  * DATA IS OPAQUE BYTES: no conversion, no rounding; NaN payloads and -0.0 survive (R9).
+ * Rows (H*D*e), strides and bases need not be multiples of 16 bytes (R29): pools where they all are
+ * take the vectorised engines; others take a narrow LDG kernel with the widest access dividing them.
  *
  * ERRORS: every call returns int, STRATA_OK (0) on success, a negative STRATA_ERR_* otherwise;
  * strata_last_error() gives a thread-local message for the last failure.  No C++ exception crosses
@@ -74,7 +76,7 @@ typedef struct strata_pool* strata_pool_t; /* opaque, library-owned */
 enum strata_status {
   STRATA_OK = 0,
   STRATA_ERR_INVALID_ARG = -1,  /* null pointer, bad size or range in a host-side value */
-  STRATA_ERR_ALIGNMENT = -2,    /* base/stride not a multiple of 16, or H*D*e % 16 != 0 (R12) */
+  STRATA_ERR_ALIGNMENT = -2,    /* a base or stride not a multiple of the element size e (R12) */
   STRATA_ERR_INDEX_RANGE = -3,  /* (validate) chunk/page index outside the pool or list */
   STRATA_ERR_DUPLICATE = -4,    /* (validate) two tokens of one call target the same destination */
   STRATA_ERR_CUDA = -5,         /* a CUDA runtime call failed (incl. an earlier async fault) */

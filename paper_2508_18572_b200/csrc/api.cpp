@@ -52,7 +52,30 @@ int strata::cuda_fail(cudaError_t e, const char* what) {
 
 namespace {
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// Widest access (16, 8, 4, 2 or 1 bytes) that divides every row size, stride, offset and base of
+// the pool: 16 selects the vectorised engines, anything else the narrow LDG kernel (R29).
+int access_granularity(const strata_pool* p) {
+  int g = 16;
+  auto fit = [&](uint64_t v) {
+    while (g > 1 && v % uint64_t(g)) g >>= 1;
+  };
+  fit(uint64_t(p->tok_bytes));
+  fit(uint64_t(p->head_bytes));
+  fit(uint64_t(p->token_stride));
+  fit(uint64_t(p->head_stride));
+  fit(uint64_t(p->page_stride));
+  fit(uint64_t(p->host_tok_stride));
+  fit(uint64_t(p->host_head_stride));
+  fit(uint64_t(p->host_head_off));
+  fit(uint64_t(p->host_kv_off));
+  fit(uint64_t(p->chunk_bytes));
+  fit(reinterpret_cast<uintptr_t>(p->host_dev));
+  for (int l = 0; l < p->d.num_layers; ++l) {
+    fit(reinterpret_cast<uintptr_t>(p->k[l]));
+    fit(reinterpret_cast<uintptr_t>(p->v[l]));
+  }
+  return g;
+}
 
 // NUMA node of the GPU's PCIe function (sysfs), -1 if unknown.
 int gpu_numa_node(int dev) {
@@ -100,30 +123,30 @@ int check_desc(const strata_pool_desc* d) {
   if (!d->k_ptrs || (!single && !d->v_ptrs)) return fail(STRATA_ERR_INVALID_ARG, "k_ptrs / v_ptrs is NULL");
   const int64_t head_bytes = int64_t(d->head_dim) * d->elem_bytes;
   const int64_t tok = head_bytes * d->num_heads;
-  if (tok % 16) return fail(STRATA_ERR_ALIGNMENT, "H*D*e = %lld is not a multiple of 16 (R12)", (long long)tok);
   if (tok > INT32_MAX / 64) return fail(STRATA_ERR_INVALID_ARG, "token row too large");
   const int64_t ts = d->token_stride ? d->token_stride : tok;
   const int64_t hs = d->head_stride ? d->head_stride : head_bytes;
   const int64_t ps = d->page_stride ? d->page_stride : d->page_size * ts;
   if (ts < 0 || hs < 0 || ps < 0) return fail(STRATA_ERR_INVALID_ARG, "negative stride");
-  if (ts % 16 || hs % 16 || ps % 16)
-    return fail(STRATA_ERR_ALIGNMENT, "device strides must be multiples of 16 (page %lld token %lld head %lld)",
-                (long long)ps, (long long)ts, (long long)hs);
-  if (hs != head_bytes && head_bytes % 16)
-    return fail(STRATA_ERR_ALIGNMENT, "non-contiguous heads need D*e %% 16 == 0");
+  // Rows need not be multiples of 16 bytes (R29: 16-byte-aligned pools take the vectorised engines,
+  // others the narrow LDG kernel), but every base and stride must be a multiple of the element size.
+  const int64_t e = d->elem_bytes;
+  if (ts % e || hs % e || ps % e)
+    return fail(STRATA_ERR_ALIGNMENT, "device strides must be multiples of the element size %lld (page %lld token "
+                "%lld head %lld)", (long long)e, (long long)ps, (long long)ts, (long long)hs);
   const int64_t Ht = d->host_heads ? d->host_heads : d->num_heads;
   if (d->host_heads < 0 || d->head_begin < 0 || d->head_begin + int64_t(d->num_heads) > Ht)
     return fail(STRATA_ERR_INVALID_ARG, "head slice [%d,%d) not inside the host tier's %lld heads", d->head_begin,
                 d->head_begin + d->num_heads, (long long)Ht);
-  if ((Ht != d->num_heads || (d->flags & STRATA_HOST_HEAD_MAJOR)) && head_bytes % 16)
-    return fail(STRATA_ERR_ALIGNMENT, "a host head slice or head-major chunks need D*e %% 16 == 0");
+  auto aligned_e = [&](const void* q) { return (reinterpret_cast<uintptr_t>(q) % uintptr_t(e)) == 0; };
   for (int l = 0; l < d->num_layers; ++l) {
     void* const vp = single ? d->k_ptrs[l] : d->v_ptrs[l];
     if (!d->k_ptrs[l] || !vp) return fail(STRATA_ERR_INVALID_ARG, "layer %d K/V pointer is NULL", l);
-    if (!aligned16(d->k_ptrs[l]) || !aligned16(vp))
-      return fail(STRATA_ERR_ALIGNMENT, "layer %d K/V pointer not 16-byte aligned", l);
+    if (!aligned_e(d->k_ptrs[l]) || !aligned_e(vp))
+      return fail(STRATA_ERR_ALIGNMENT, "layer %d K/V pointer not aligned to the element size", l);
   }
-  if (d->host_base && !aligned16(d->host_base)) return fail(STRATA_ERR_ALIGNMENT, "host_base not 16-byte aligned");
+  if (d->host_base && !aligned_e(d->host_base))
+    return fail(STRATA_ERR_ALIGNMENT, "host_base not aligned to the element size");
   const int64_t htok = head_bytes * Ht;   // one token of one chunk-layer-kv block, all host heads
   const int64_t chunk = int64_t(d->num_layers) * nkv * d->chunk_tokens * htok;
   if (chunk / htok / nkv / d->chunk_tokens != d->num_layers || d->num_chunks > INT64_MAX / chunk)
@@ -272,6 +295,7 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
     return cuda_fail(e, "cudaHostGetDevicePointer");
   }
   p->host_dev = static_cast<char*>(dptr);
+  p->gran = access_granularity(p);
 
   p->events.assign(size_t(kEventRing) * (d->num_layers + 1), nullptr);
   for (auto& ev : p->events) {

@@ -61,6 +61,7 @@ struct XferParams {
   const int32_t* dev_pages;
   int32_t ntok;                 // tokens in this launch
   int32_t nkv;                  // KV buffers per layer: 2 (K, V) or 1 (MLA latent); rows = nkv*ntok
+  int32_t gran;                 // 16: vectorised kernels; 8/4/2/1: the narrow LDG kernel (R29)
   ReqTable rt;
 };
 
@@ -114,6 +115,7 @@ struct strata_pool {
   std::vector<void*> k, v;
   int64_t tok_bytes, head_bytes, chunk_bytes;
   int32_t nkv = 2;                    // KV buffers per layer (1: STRATA_POOL_SINGLE_KV)
+  int32_t gran = 16;                  // widest access dividing every row, stride and base (R29)
   int32_t host_heads = 0, head_begin = 0;   // Ht, h0 (R28)
   bool head_major = false;
   int64_t host_kv_off = 0, host_tok_stride = 0, host_head_off = 0, host_head_stride = 0;
@@ -211,9 +213,13 @@ constexpr int kDefaultCtasLdg = 2;
 // where the bandwidth is already sufficient and overhead must be minimized".  On B200
 // one 1024-thread CTA offloads 39-40 GB/s and costs a co-running decode ~5 % instead of ~12 %.
 constexpr int kDefaultCtasLdgOffload = 1;
+// The narrow kernel (R29) moves one row segment per warp at a time, latency-bound: it needs many
+// warps in flight whatever the direction.
+constexpr int kDefaultCtasNarrow = 64;
 constexpr int kDefaultThreadsLdg = 1024;   // host-read throughput of an SM scales with its warps
 constexpr int64_t kDmaMinLayerBytes = int64_t(4) << 20;
 constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;
+constexpr int64_t kDmaMinLoadRun = int64_t(24) << 10;   // default engine: DMA loads need >= 24 KiB runs
 constexpr int kDefaultUnroll = 8;
 constexpr int kDefaultCtasTma = 2;   // warp-specialised ring: 51.0 GB/s at 2 CTAs (sweep_tma_ws15.jsonl)
 constexpr int kTmaStageTarget = 32 << 10;

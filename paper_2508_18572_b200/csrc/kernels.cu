@@ -506,6 +506,54 @@ __global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel
 }
 
 // ---------------------------------------------------------------------------------------------
+// Narrow LDG kernel (R29): pools whose rows, strides or bases are not 16-byte multiples.  Each warp
+// takes one (row, head) segment at a time — D*e bytes contiguous on both sides, or the whole row
+// when its heads are adjacent on both sides — and its lanes copy W-byte words (W = the pool's access
+// granularity: 8, 4, 2 or 1).  A fallback for geometries the vectorised engines cannot take.
+template <int W>
+struct Word;
+template <> struct Word<8> { using T = unsigned long long; };
+template <> struct Word<4> { using T = unsigned int; };
+template <> struct Word<2> { using T = unsigned short; };
+template <> struct Word<1> { using T = unsigned char; };
+
+template <int W, int DIR>
+__global__ void __launch_bounds__(1024) ldg_narrow_kernel(const __grid_constant__ XferParams p) {
+  using T = typename Word<W>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
+  const bool whole = (p.head_stride == p.head_bytes && p.host_head_stride == p.head_bytes) || p.H == 1;
+  const int nseg = whole ? 1 : p.H;
+  const int64_t seg_bytes = whole ? p.tok_bytes : p.head_bytes;
+  const int64_t nwords = seg_bytes / W;
+  for (int64_t s = warp; s < nrows * nseg; s += nwarps) {
+    const int64_t row = s / nseg;
+    const int h = static_cast<int>(s - row * nseg);
+    char* hp = nullptr;
+    char* dp = nullptr;
+    row_finish(p, row_fetch(p, row), hp, dp);
+    hp += static_cast<int64_t>(h) * p.host_head_stride;
+    dp += static_cast<int64_t>(h) * p.head_stride;
+    const T* src = reinterpret_cast<const T*>(DIR == 0 ? hp : dp);
+    T* dst = reinterpret_cast<T*>(DIR == 0 ? dp : hp);
+    for (int64_t w = lane; w < nwords; w += 32) dst[w] = src[w];
+  }
+}
+
+template <int DIR>
+cudaError_t ldg_narrow_launch(const XferParams& p, int ctas, int threads, cudaStream_t s) {
+  switch (p.gran) {
+    case 8: ldg_narrow_kernel<8, DIR><<<ctas, threads, 0, s>>>(p); break;
+    case 4: ldg_narrow_kernel<4, DIR><<<ctas, threads, 0, s>>>(p); break;
+    case 2: ldg_narrow_kernel<2, DIR><<<ctas, threads, 0, s>>>(p); break;
+    default: ldg_narrow_kernel<1, DIR><<<ctas, threads, 0, s>>>(p); break;
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
 __global__ void validate_kernel(const __grid_constant__ ValidateParams v) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < v.ntok; g += stride) {
@@ -570,6 +618,7 @@ static bool dev_contig(const XferParams& p) { return p.head_stride == p.head_byt
 static bool host_contig(const XferParams& p) { return p.host_head_stride == p.head_bytes || p.H == 1; }
 
 cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s) {
+  if (p.gran < 16) return dir == 0 ? ldg_narrow_launch<0>(p, ctas, threads, s) : ldg_narrow_launch<1>(p, ctas, threads, s);
   const bool contig = dev_contig(p), hcontig = host_contig(p);
   if (threads > 512) unroll = 4;  // U=8 needs > 64 registers per thread
   if (unroll == 4) return dir == 0 ? ldg_launch<4, 0>(p, contig, hcontig, ctas, threads, s)

@@ -286,6 +286,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.host_chunks = x->host_chunks;
   xp.dev_pages = x->dev_pages;
   xp.nkv = p->nkv;
+  xp.gran = p->gran;
 
   int engine = x->engine;
   if (engine == STRATA_ENGINE_DEFAULT) {
@@ -294,8 +295,13 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     // amortised and the zero-copy LDG kernel wins.  Without a host mirror of the chunk list only
     // the kernel engines can run.
     // (Offloads group layers into >= 128 KiB runs inside the DMA engine, see transfer_dma.)
+    // Loads copy one chunk-layer per run (per head for head-major tiers); below ~24 KiB a run the
+    // copy engines fall behind the SM path (72-byte rows at C = 64: 9 KiB runs, DMA 24 vs LDG 33.5
+    // GB/s; tools/narrow_probe.py).  Offloads group layers into >= 128 KiB runs anyway.
     const int64_t layer_bytes = p->nkv * plan.total_tokens * p->tok_bytes;
-    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes && dma_runs_ok(p);
+    const int64_t run = int64_t(p->nkv) * p->d.chunk_tokens * (p->head_major ? p->head_bytes : p->tok_bytes);
+    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes && dma_runs_ok(p) &&
+                     (dir == 1 || run >= kDmaMinLoadRun);
     engine = dma ? STRATA_ENGINE_DMA : STRATA_ENGINE_LDG;
   }
   // the copy engines need long host runs: a token-major tier read in a head slice (Ht > H) has
@@ -321,8 +327,9 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     if (ticket) *ticket = t;
     return STRATA_OK;
   }
-  // the TMA rings stage whole host rows: a head-major tier with > 1 head per GPU has none
-  if ((engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK) && !p->host_row_contig())
+  // the TMA rings stage whole host rows in 16-byte units: a head-major tier with > 1 head per GPU
+  // has no whole rows, a pool whose rows / strides are not 16-byte multiples (R29) no 16-byte units
+  if ((engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK) && (!p->host_row_contig() || p->gran < 16))
     engine = STRATA_ENGINE_LDG;
   const bool tma = engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK;
   // TMA engine geometry: rows per stage (<= 32 lanes), stage bytes, depth
@@ -343,10 +350,14 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   }
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;   // U=8 is compiled for <= 512 threads
-  xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows (amortised index math)
+  // lane t fetches row t; the warp then streams the 32 rows (amortised index math).  The narrow
+  // kernel (R29) takes one row per warp, so its grid is sized per row.
+  xp.rows_per_group = p->gran < 16 ? 1 : 32;
   int ctas = x->num_ctas ? x->num_ctas
-                         : engine == STRATA_ENGINE_LDG ? (dir == 0 ? kDefaultCtasLdg : kDefaultCtasLdgOffload)
-                                                       : kDefaultCtasTma;
+             : engine != STRATA_ENGINE_LDG ? kDefaultCtasTma
+             : p->gran < 16                ? kDefaultCtasNarrow
+             : dir == 0                    ? kDefaultCtasLdg
+                                           : kDefaultCtasLdgOffload;
   // small token rows shrink a TMA stage (<= 32 rows); keep ~64 KiB per stage-CTA in flight by
   // spreading over more CTAs (70B TP=8: 256 B rows -> 8 KiB stages -> 16 CTAs)
   if (!x->num_ctas && engine != STRATA_ENGINE_LDG && xp.tma_stage_bytes > 0)
@@ -372,7 +383,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const int64_t fgroups = plan.batches.empty() ? 0
                               : (int64_t(p->nkv) * plan.batches[0].ntok + xp.rows_per_group - 1) / xp.rows_per_group;
   const int fctas = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctas, (fgroups * 32 + threads - 1) / threads)));
-  if (engine == STRATA_ENGINE_LDG && plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 &&
+  if (engine == STRATA_ENGINE_LDG && p->gran == 16 && plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 &&
       (fctas >= 2 || fused_mode() == 2) && L <= kMaxFusedLayers && fused_mode() && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
       cap == cudaStreamCaptureStatusNone && ensure_fused(p)) {
     const Batch& b = plan.batches[0];

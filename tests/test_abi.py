@@ -84,10 +84,9 @@ def _register(lib, desc):
     ("num_layers", 0, _lib.STRATA_ERR_INVALID_ARG),
     ("page_size", 0, _lib.STRATA_ERR_INVALID_ARG),
     ("num_chunks", 0, _lib.STRATA_ERR_INVALID_ARG),
-    ("head_dim", 3, _lib.STRATA_ERR_ALIGNMENT),          # H*D*e = 12 bytes, not a multiple of 16 (R12)
-    ("token_stride", 8 + 256, _lib.STRATA_ERR_ALIGNMENT),
-    ("page_stride", 24, _lib.STRATA_ERR_ALIGNMENT),
-    ("host_base", 0x1008, _lib.STRATA_ERR_ALIGNMENT),
+    ("token_stride", 1 + 256, _lib.STRATA_ERR_ALIGNMENT),   # not a multiple of e = 2 (R29)
+    ("page_stride", 25, _lib.STRATA_ERR_ALIGNMENT),
+    ("host_base", 0x1001, _lib.STRATA_ERR_ALIGNMENT),
     ("num_pages", 1 << 31, _lib.STRATA_ERR_INVALID_ARG),
 ])
 def test_register_rejects_bad_descriptor(lib, field, value, code):
@@ -103,9 +102,22 @@ def test_register_rejects_null_and_misaligned_layer_ptrs(lib):
     k = (ctypes.c_void_p * 2)(0x10000, 0)
     desc, keep = _desc(k_ptrs=ctypes.cast(k, ctypes.POINTER(ctypes.c_void_p)))
     assert _register(lib, desc)[0] == _lib.STRATA_ERR_INVALID_ARG
-    k = (ctypes.c_void_p * 2)(0x10000, 0x10004)
+    k = (ctypes.c_void_p * 2)(0x10000, 0x10003)   # not a multiple of the 2-byte element
     desc, keep = _desc(k_ptrs=ctypes.cast(k, ctypes.POINTER(ctypes.c_void_p)))
     assert _register(lib, desc)[0] == _lib.STRATA_ERR_ALIGNMENT
+
+
+@pytest.mark.parametrize("field,value", [("head_dim", 3), ("token_stride", 8 + 256), ("page_stride", 24),
+                                         ("host_base", 0x1008)])
+def test_rows_and_strides_need_not_be_16_byte_multiples(lib, field, value):
+    """R29: 12-byte rows, 8-byte-aligned strides and bases pass the host-side checks (the narrow LDG
+    kernel takes them); on a box without a GPU registration then stops at the first CUDA call."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    desc, keep = _desc(**{field: value})
+    rc, h = _register(lib, desc)
+    assert rc not in (_lib.STRATA_ERR_ALIGNMENT, _lib.STRATA_ERR_INVALID_ARG), lib.strata_last_error()
 
 
 def test_valid_descriptor_without_gpu_fails_in_cuda(lib):
