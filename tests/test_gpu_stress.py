@@ -1,4 +1,5 @@
 """Randomised stress parity (slow): 1500 cases drawn over EVERY axis at once — engine, SM quota,
+row width (16-byte multiples and narrow rows, R29),
 direction, page / chunk size, ragged counts and offsets, fragmentation, device row layout (NHD, HND,
 padded), one or two KV buffers (R27), host head slices and head-major chunks (R28), consecutive or
 permuted host chunks (strided copy runs), layer groups, layer ranges — each bit-exact against the
@@ -30,7 +31,8 @@ def _case(i):
     H = int(rng.choice([h for h in (1, 2, 4, 8) if h <= Ht]))
     h0 = int(rng.integers(0, Ht - H + 1))
     head_major = bool(rng.integers(0, 2)) and Ht > 1
-    D = int(rng.choice([64, 128, 576] if H == 1 else [64, 128]))
+    # 16-byte rows mostly; a fifth of the cases take narrow rows (R29: 3..72-byte heads)
+    D = int(rng.choice([3, 10, 36, 72])) if rng.random() < 0.2 else int(rng.choice([64, 128, 576] if H == 1 else [64, 128]))
     e = int(rng.choice([1, 2]))
     P = int(rng.choice([1, 2, 8, 16, 64]))
     C = int(rng.choice([1, 8, 64, 128]))
@@ -42,10 +44,10 @@ def _case(i):
                  head_major=head_major)
     tok = g.token_bytes
     layout = rng.choice(["nhd", "hnd", "padded"])
-    if layout == "hnd" and H > 1:
+    if layout == "hnd" and H > 1 and (D * e) % e == 0:
         strides = (H * P * D * e, D * e, P * D * e)
     elif layout == "padded":
-        strides = (P * (tok + 32) + 48, tok + 32, D * e)
+        strides = (P * (tok + 2 * e) + 4 * e, tok + 2 * e, D * e)
     else:
         strides = None
     q = kvgen.make_requests(rng, ns, P, C, num_pages, num_chunks, offsets=True,
@@ -60,8 +62,6 @@ def _case(i):
 def test_stress(i):
     f = _case(i)
     g, q = f["g"], f["q"]
-    if g.D * g.e % 16:
-        pytest.skip("row not a multiple of 16 bytes")
     c = GpuCase(g, q, strides=f["strides"], seed=i, dev_fill="random" if f["offload"] else "canary")
     try:
         kw = dict(engine=f["engine"], num_ctas=f["ctas"], layer_group=f["group"])
