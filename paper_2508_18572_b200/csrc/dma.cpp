@@ -359,7 +359,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   cudaError_t e;
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;
-  xp.rows_per_group = p->gran < 16 ? 1 : 32;   // LDG: 32-row warp groups; narrow kernel: a row per warp
+  xp.rows_per_group = 32;   // lane t fetches row t; the warp then streams the 32 rows
   const int ctas = x->num_ctas ? x->num_ctas : p->gran < 16 ? kDefaultCtasNarrow : kDefaultCtasScatter;
   // the scatter / gather kernel sees the staging slots as a compact host tier (chunk = slot)
   xp.chunk_bytes = static_cast<int64_t>(m.gunit);

@@ -62,6 +62,8 @@ struct XferParams {
   int32_t ntok;                 // tokens in this launch
   int32_t nkv;                  // KV buffers per layer: 2 (K, V) or 1 (MLA latent); rows = nkv*ntok
   int32_t gran;                 // 16: vectorised kernels; 8/4/2/1: the narrow LDG kernel (R29)
+  int32_t wpr, wph;             // narrow kernel: gran-byte words per row / per head
+  uint32_t wpr_magic, wph_magic;   // their multiply-high divisors (0 = divide)
   ReqTable rt;
 };
 
@@ -213,9 +215,10 @@ constexpr int kDefaultCtasLdg = 2;
 // where the bandwidth is already sufficient and overhead must be minimized".  On B200
 // one 1024-thread CTA offloads 39-40 GB/s and costs a co-running decode ~5 % instead of ~12 %.
 constexpr int kDefaultCtasLdgOffload = 1;
-// The narrow kernel (R29) moves one row segment per warp at a time, latency-bound: it needs many
-// warps in flight whatever the direction.
-constexpr int kDefaultCtasNarrow = 64;
+// The narrow kernel (R29) streams 8-byte or smaller words (half the bytes in flight per warp of the
+// 16-byte LDG engine): it saturates from 16 CTAs (72 / 100 / 120-byte rows: 46.4 / 46.6 / 48.2 GB/s;
+// profiles/r01/final/narrow_probe.jsonl).
+constexpr int kDefaultCtasNarrow = 16;
 constexpr int kDefaultThreadsLdg = 1024;   // host-read throughput of an SM scales with its warps
 constexpr int64_t kDmaMinLayerBytes = int64_t(4) << 20;
 constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;

@@ -506,10 +506,11 @@ __global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel
 }
 
 // ---------------------------------------------------------------------------------------------
-// Narrow LDG kernel (R29): pools whose rows, strides or bases are not 16-byte multiples.  Each warp
-// takes one (row, head) segment at a time — D*e bytes contiguous on both sides, or the whole row
-// when its heads are adjacent on both sides — and its lanes copy W-byte words (W = the pool's access
-// granularity: 8, 4, 2 or 1).  A fallback for geometries the vectorised engines cannot take.
+// Narrow LDG kernel (R29): pools whose rows, strides or bases are not 16-byte multiples.  Same
+// shape as the LDG engine: a warp owns a group of 32 rows, lane t fetches row t's indices one group
+// ahead, and the warp streams the group's W-byte words (W = the pool's access granularity: 8, 4, 2
+// or 1) with 4 independent loads per lane, row addresses broadcast by __shfl_sync; word -> (row,
+// head, offset) by multiply-high when the divisors allow it.
 template <int W>
 struct Word;
 template <> struct Word<8> { using T = unsigned long long; };
@@ -517,28 +518,62 @@ template <> struct Word<4> { using T = unsigned int; };
 template <> struct Word<2> { using T = unsigned short; };
 template <> struct Word<1> { using T = unsigned char; };
 
+__device__ __forceinline__ int div_by(int n, int d, uint32_t magic) {
+  return magic ? static_cast<int>(__umulhi(static_cast<unsigned>(n), magic)) : n / d;
+}
+
 template <int W, int DIR>
 __global__ void __launch_bounds__(1024) ldg_narrow_kernel(const __grid_constant__ XferParams p) {
   using T = typename Word<W>::T;
+  constexpr int U = 4;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
-  const bool whole = (p.head_stride == p.head_bytes && p.host_head_stride == p.head_bytes) || p.H == 1;
-  const int nseg = whole ? 1 : p.H;
-  const int64_t seg_bytes = whole ? p.tok_bytes : p.head_bytes;
-  const int64_t nwords = seg_bytes / W;
-  for (int64_t s = warp; s < nrows * nseg; s += nwarps) {
-    const int64_t row = s / nseg;
-    const int h = static_cast<int>(s - row * nseg);
+  const int64_t ngroups = (nrows + 31) / 32;
+  const int wpr = p.wpr, wph = p.wph;
+  const bool dcont = p.head_stride == p.head_bytes || p.H == 1;
+  const bool hcont = p.host_head_stride == p.head_bytes || p.H == 1;
+  const bool scont = DIR == 0 ? hcont : dcont, tcont = DIR == 0 ? dcont : hcont;
+  const int64_t sstride = DIR == 0 ? p.host_head_stride : p.head_stride;
+  const int64_t tstride = DIR == 0 ? p.head_stride : p.host_head_stride;
+  auto word_addr = [&](uint64_t base, int w, bool cont, int64_t stride) {
+    if (cont) return base + static_cast<uint64_t>(w) * W;
+    const int h = div_by(w, wph, p.wph_magic);
+    return base + h * stride + static_cast<uint64_t>(w - h * wph) * W;
+  };
+  auto fetch = [&](int64_t gi) {
+    const int64_t row = gi * 32 + lane;
+    return (gi < ngroups && row < nrows) ? row_fetch(p, row) : row_none();
+  };
+  RowIdx nx = fetch(warp);
+  for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+    const RowIdx cur = nx;
+    nx = fetch(gi + nwarps);
     char* hp = nullptr;
     char* dp = nullptr;
-    row_finish(p, row_fetch(p, row), hp, dp);
-    hp += static_cast<int64_t>(h) * p.host_head_stride;
-    dp += static_cast<int64_t>(h) * p.head_stride;
-    const T* src = reinterpret_cast<const T*>(DIR == 0 ? hp : dp);
-    T* dst = reinterpret_cast<T*>(DIR == 0 ? dp : hp);
-    for (int64_t w = lane; w < nwords; w += 32) dst[w] = src[w];
+    if (cur.kv >= 0) row_finish(p, cur, hp, dp);
+    const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
+    const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
+    const int nr = static_cast<int>(min(static_cast<int64_t>(32), nrows - gi * 32));
+    const int total = nr * wpr;
+    for (int base = 0; base < total; base += 32 * U) {
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * 32 + lane;
+        const int r = div_by(idx, wpr, p.wpr_magic);
+        const uint64_t sb = __shfl_sync(kFull, my_src, r & 31);
+        if (idx < total) v[u] = __ldg(reinterpret_cast<const T*>(word_addr(sb, idx - r * wpr, scont, sstride)));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * 32 + lane;
+        const int r = div_by(idx, wpr, p.wpr_magic);
+        const uint64_t db = __shfl_sync(kFull, my_dst, r & 31);
+        if (idx < total) *reinterpret_cast<T*>(word_addr(db, idx - r * wpr, tcont, tstride)) = v[u];
+      }
+    }
   }
 }
 

@@ -287,6 +287,10 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.dev_pages = x->dev_pages;
   xp.nkv = p->nkv;
   xp.gran = p->gran;
+  xp.wpr = static_cast<int32_t>(p->tok_bytes / p->gran);
+  xp.wph = static_cast<int32_t>(p->head_bytes / p->gran);
+  xp.wpr_magic = (xp.wpr & (xp.wpr - 1)) ? div_magic(xp.wpr, 32 * xp.wpr + 32 * 4) : 0;
+  xp.wph_magic = (xp.wph & (xp.wph - 1)) ? div_magic(xp.wph, xp.wpr) : 0;
 
   int engine = x->engine;
   if (engine == STRATA_ENGINE_DEFAULT) {
@@ -352,7 +356,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;   // U=8 is compiled for <= 512 threads
   // lane t fetches row t; the warp then streams the 32 rows (amortised index math).  The narrow
   // kernel (R29) takes one row per warp, so its grid is sized per row.
-  xp.rows_per_group = p->gran < 16 ? 1 : 32;
+  xp.rows_per_group = 32;
   int ctas = x->num_ctas ? x->num_ctas
              : engine != STRATA_ENGINE_LDG ? kDefaultCtasTma
              : p->gran < 16                ? kDefaultCtasNarrow

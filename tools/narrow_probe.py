@@ -25,17 +25,19 @@ def main():
                            k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
         reqs = st.Requests.from_kvgen(q)
         nbytes = 2 * g.L * 32768 * g.token_bytes
-        for eng in (0, 1):
+        quotas = [int(x) for x in os.environ.get("NARROW_CTAS", "0").split(",")]
+        for eng, c in [(0, 0)] + [(1, c) for c in quotas]:
             for d, fn in (("load", pool.load), ("offload", pool.offload)):
-                fn(reqs, stream=io, engine=eng)
+                fn(reqs, stream=io, engine=eng, num_ctas=c)
                 torch.cuda.synchronize()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(io)
                 for _ in range(3):
-                    fn(reqs, stream=io, engine=eng)
+                    fn(reqs, stream=io, engine=eng, num_ctas=c)
                 b.record(io)
                 b.synchronize()
-                print(json.dumps({"row_bytes": g.token_bytes, "engine": {0: "default", 1: "ldg"}[eng], "dir": d,
+                print(json.dumps({"row_bytes": g.token_bytes, "engine": {0: "default", 1: "ldg"}[eng], "ctas": c,
+                                  "dir": d,
                                   "used": pool.counters()["last_engine"],
                                   "gbs": round(3 * nbytes / (a.elapsed_time(b) / 1e3) / 1e9, 2)}), flush=True)
         pool.close()
