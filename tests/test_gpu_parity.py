@@ -255,9 +255,15 @@ def test_dma_engine_needs_host_list():
         c.close()
 
 
-def test_baselines_match_oracle():
-    """The copy-engine baselines produce the same bytes (a library-routine pin on hardware)."""
-    g = Geometry(3, 2, 64, 2, 4, 16, 96, 24)
+@pytest.mark.parametrize("variant", ["gqa", "mla", "head_major_slice", "token_major_slice", "narrow"])
+def test_baselines_match_oracle(variant):
+    """The copy-engine baselines produce the same bytes (a library-routine pin on hardware), on the
+    paper's GQA pools and on every pool variant (R27-R29)."""
+    g = {"gqa": Geometry(3, 2, 64, 2, 4, 16, 96, 24),
+         "mla": Geometry(3, 1, 576, 2, 4, 16, 96, 24, kv=1),
+         "head_major_slice": Geometry(3, 2, 64, 2, 4, 16, 96, 24, Ht=6, h0=3, head_major=True),
+         "token_major_slice": Geometry(3, 2, 64, 2, 4, 16, 96, 24, Ht=4, h0=1),
+         "narrow": Geometry(3, 3, 10, 2, 4, 16, 96, 24)}[variant]
     rng = kvgen.rng_for(8)
     q = kvgen.make_requests(rng, [37, 100, 5], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
     for fn in (st.strata_baseline_memcpy_pages, st.strata_baseline_memcpy_batch):
