@@ -16,9 +16,18 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2508_18572_b200 as st  # noqa: E402
 
 
+VARIANTS = {
+    "gqa": Geometry(4, 8, 128, 2, 1, 64, 12000, 200),                      # 8K tokens: 32 MiB per layer
+    "mla": Geometry(4, 1, 576, 2, 1, 64, 12000, 200, kv=1),                # R27
+    "head_major_slice": Geometry(4, 1, 128, 2, 1, 64, 12000, 200, Ht=8, h0=5, head_major=True),   # R28
+    "narrow": Geometry(4, 1, 72, 1, 1, 256, 12000, 60),                     # R29
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
 @pytest.mark.parametrize("engine", [st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_DMA])
-def test_load_replays_from_cuda_graph(engine):
-    g = Geometry(4, 8, 128, 2, 1, 64, 12000, 200)          # 8K tokens: 32 MiB per layer
+def test_load_replays_from_cuda_graph(engine, variant):
+    g = VARIANTS[variant]
     q = kvgen.make_requests(kvgen.rng_for(6), [8000, 1500], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
     c = GpuCase(g, q)
     try:
@@ -38,7 +47,7 @@ def test_load_replays_from_cuda_graph(engine):
         torch.cuda.synchronize()
         c.check_load(0, g.L)
         # the graph reads the host tier at replay time
-        c.pool.host[:] = kvgen.random_bytes(kvgen.rng_for(99), g.host_bytes)
+        c.pool.host[: g.host_bytes] = kvgen.random_bytes(kvgen.rng_for(99), g.host_bytes)
         graph.replay()
         torch.cuda.synchronize()
         c.check_load(0, g.L)
