@@ -17,6 +17,10 @@
 //   tma_ws_load_kernel  zero-copy TMA: one producer warp issues one cp.async.bulk per contiguous
 //                       host run into a shared-memory ring; 15 consumer warps drain it to the pages.
 //   tma_kernel          zero-copy TMA, single warp, bulk copies on both sides of the ring.
+//   ldg_fused_kernel    the LDG engine over every layer of an operation in one launch, per-layer
+//                       completion published as device flags.
+//   ldg_narrow_kernel   the LDG engine's shape over 8/4/2/1-byte words, for pools whose rows,
+//                       strides or bases are not 16-byte multiples (R29).
 // Measured on the B200 box (profiles/r01): SM-issued host reads top out at 51.4 GB/s (92.6 % of the
 // 55.5 GB/s pinned memcpy) whatever the instruction or cache hint; per SM they scale with resident
 // warps (~1 KiB in flight per warp), so the LDG engine uses 1024-thread CTAs and reaches 50.3 GB/s
