@@ -47,6 +47,16 @@
  * STRATA_VALIDATE (or env STRATA_VALIDATE=1): a device check kernel plus a stream synchronisation.
  * Asynchronous kernel faults surface as STRATA_ERR_CUDA on a later call.
  *
+ * ENVIRONMENT (defaults are the measured choices of DESIGN.md §6; the knobs exist for A/B runs):
+ *   STRATA_VALIDATE=1          as the STRATA_VALIDATE pool flag, for every pool
+ *   STRATA_LDG_FUSED=0|force   per-layer LDG launches only | fuse even 1-CTA grids (default: fuse >= 2)
+ *   STRATA_COPY_STREAMS=n      copy streams of the DMA engine per direction (default 1)
+ *   STRATA_STAGE_MB=n          DMA staging slot size (default 128)
+ *   STRATA_DMA_EDGE_SPLIT=n    first / last layer in n times smaller pieces (default 4; 1 = off)
+ *   STRATA_DMA_ORDERED=0       drop the per-piece barrier between copy streams (default on)
+ *   STRATA_DMA_STRIDED=0       one copy per chunk instead of strided runs of consecutive chunks
+ *   STRATA_DMA_NO_BATCH=1      plain cudaMemcpyAsync instead of cudaMemcpyBatchAsync
+ *
  * THREADING: a pool handle is single-writer (one thread at a time); distinct handles are
  * independent.  Operations of one handle may be in flight at once on different streams (e.g. a
  * load and an offload: both directions of the link); the library orders their use of its internal
