@@ -1,0 +1,62 @@
+"""The north_star target as a test (slow): on the Llama-3.1-8B 32K workload, strata_load moves at
+least 85 % of the live contiguous host->device memcpy rate of the same host tier at page size 1 and
+16 — with the default engine and with the paper's own design (zero-copy LDG, 2 CTAs) — and its
+per-layer events complete in layer order.  A ratio against the link measured in the same process,
+so a slow box moves both sides."""
+import statistics
+
+import pytest
+
+import kvgen
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2508_18572_b200 as st  # noqa: E402
+
+
+def _median_ms(fn, io, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(io)
+        fn()
+        b.record(io)
+        b.synchronize()
+        out.append(a.elapsed_time(b))
+    return statistics.median(out)
+
+
+@pytest.mark.parametrize("P", [1, 16])
+def test_load_reaches_85_percent_of_the_link(P):
+    g = kvgen.geometry("llama8b_32k", P=P)
+    q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks)
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+    try:
+        reqs = st.Requests.from_kvgen(q)
+        io = torch.cuda.Stream()
+        nbytes = 2 * g.L * q.total_tokens * g.token_bytes
+        scratch = torch.empty(nbytes // g.L, dtype=torch.uint8, device="cuda")
+
+        def link():
+            for _ in range(g.L):
+                st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, scratch.numel(), io)
+        link_gbs = nbytes / (_median_ms(link, io) / 1e3) / 1e9
+        for engine in (st.STRATA_ENGINE_DEFAULT, st.STRATA_ENGINE_LDG):
+            gbs = nbytes / (_median_ms(lambda: pool.load(reqs, stream=io, engine=engine), io) / 1e3) / 1e9
+            assert gbs >= 0.85 * link_gbs, (engine, P, gbs, link_gbs)
+        t = pool.load(reqs, stream=io)
+        done = [pool.layer_elapsed_ms(t, l) for l in range(g.L)]
+        assert all(b >= a for a, b in zip(done, done[1:])), done
+        assert done[0] < done[-1] / 4, "layer 0 must complete long before the last layer (overlap)"
+    finally:
+        pool.close()
