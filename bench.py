@@ -2,14 +2,17 @@
 """bench.py — KV load throughput of libstrata on B200 (BASELINE.json metric).
 
 One "step" = one strata_load of the whole cached prefix, every layer (all §8(a) rows: planning,
-index fetch + layout transform, host->HBM movement, per-layer events) — for the default workload
-BASELINE.json configs[1]: Llama-3.1-8B geometry (32 layers, 8 KV heads, d=128, bf16), a 32K-token
-prefix, page size 1, randomly fragmented pages, 4 GiB per step (> 126 MB L2, so no flush needed).
+index fetch + layout transform, host->HBM movement, per-layer completion flags/events) — for the
+default workload BASELINE.json configs[1]: Llama-3.1-8B geometry (32 layers, 8 KV heads, d=128,
+bf16), a 32K-token prefix, page size 1, randomly fragmented pages, 4 GiB per step (> 126 MB L2, so no
+flush is needed).  The default engine is the hand-written zero-copy ring kernel (csrc/ring.cu):
+TMA bulk reads of the page-first host runs through the tier's UVA mapping, LSU scatter to the pages.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl strata|reference] [--config ...] [--page-size P]
 
-Multi-GPU (torchrun): every rank loads its own replica workload over its own PCIe link (weak
-scaling, no data-path collective; NCCL only for the start barrier and the max-over-ranks timing).
+Multi-GPU (torchrun): every rank loads its own workload over its own PCIe link (weak scaling, no
+data-path collective; torch.distributed only for barriers and the timing reductions).  Each rank is
+pinned to its GPU's NUMA node; its link ceiling is measured concurrently with the other ranks'.
 Rank 0 prints ONE JSON line.  ``--impl reference`` times the CPU oracle (oracle/, test
 infrastructure) on the host cores instead.
 """
@@ -33,36 +36,39 @@ import numpy as np  # noqa: E402
 import kvgen  # noqa: E402
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
-ENGINE_NAMES = {0: "default", 1: "ldg", 2: "tma", 3: "tma_bulk", 4: "dma"}
-SM_ZERO_COPY_CEILING = 51.44   # GB/s, profiles/r01/probe.jsonl: SM-issued host reads, best of the sweep
+ENGINE_NAMES = {0: "default", 1: "ldg", 2: "ring", 3: "tma_bulk", 4: "dma"}
 PATH_DESC = {
-    "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (cudaMemcpyBatchAsync on one in-order copy stream) "
-           "into an HBM staging slot + ldg_kernel scatter to the pages; one event per layer",
-    "ldg": "ldg_kernel, zero-copy LDG/STG from mapped host memory, one launch + event per layer",
-    "tma": "tma_ws_load_kernel, zero-copy cp.async.bulk ring, one launch + event per layer",
-    "tma_bulk": "tma_kernel, zero-copy cp.async.bulk ring, one launch + event per layer",
+    "ring": "ring_load_kernel (csrc/ring.cu): ONE persistent launch for all layers; per CTA a TMA producer warp "
+            "(one cp.async.bulk per page-first host run of <= 32 KiB, from the UVA-mapped tier) + 8 LSU scatter "
+            "warps (16-byte st.global to the pages); per-layer completion flags -> layer events",
+    "ldg": "ldg_fused_kernel (csrc/kernels.cu): zero-copy 16-byte LDG/STG register staging, one launch for all layers",
+    "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (cudaMemcpyBatchAsync) into an HBM "
+           "staging slot + ldg_kernel scatter to the pages",
+    "tma_bulk": "tma_kernel (csrc/kernels.cu): one warp per CTA, cp.async.bulk on both sides of a smem ring",
 }
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="strata", choices=["strata", "reference"])
     ap.add_argument("--config", default="llama8b_32k", choices=list(kvgen.CONFIGS))
     ap.add_argument("--page-size", type=int, default=None)
     ap.add_argument("--chunk-tokens", type=int, default=None,
                     help="host chunk size C (the host tier keeps the same token capacity)")
-    ap.add_argument("--engine", type=int, default=0, help="0 default, 1 LDG, 2 TMA")
+    ap.add_argument("--engine", type=int, default=0, help="0 default (ring), 1 LDG, 2 ring, 3 TMA bulk, 4 DMA")
     ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--layer-group", type=int, default=0, help="DMA engine: layers per copy run (0 = library default)")
     ap.add_argument("--frag", default="perm", choices=["perm", "churn"])
     ap.add_argument("--chunk-frag", default="perm", choices=["perm", "identity"],
                     help="host chunk lists: a random permutation of the tier, or consecutive chunks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the side measurements (P=16, offload, other engines, contiguous ceiling)")
     ap.add_argument("--seed", type=int, default=1)
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -72,10 +78,10 @@ def dist_env():
     return rank, world, local
 
 
-def workload(args, rank: int, world: int):
+def workload(args, rank: int, world: int, P=None):
     """Per-rank geometry + request tables (replicas of the config; the TP config is already the
     per-rank head slice)."""
-    g = kvgen.geometry(args.config, P=args.page_size)
+    g = kvgen.geometry(args.config, P=P if P is not None else args.page_size)
     if args.chunk_tokens and args.chunk_tokens != g.C:
         g = dataclasses.replace(g, C=args.chunk_tokens, num_chunks=-(-g.num_chunks * g.C // args.chunk_tokens))
     if g.host_heads > g.H:   # a shared tier holding every KV head: this rank moves head slice `rank`
@@ -144,10 +150,48 @@ class ClockSampler:
                 "samples": len(sm), "pcie_link": sorted(links)}
 
 
+# ------------------------------------------------------------------------------------------------
+# Multi-rank reductions (torch.distributed; CPU tensors under gloo, CUDA tensors under NCCL).  Pure
+# functions of per-rank numbers so that tests/test_multiproc.py runs them under gloo.
+def reduce_max(dist, world, x: float, device="cpu") -> float:
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_floats(dist, world, xs, device="cpu"):
+    """[rank][field] for a per-rank list of floats (every rank gets every row)."""
+    import torch
+    t = torch.tensor([float(v) for v in xs], dtype=torch.float64, device=device)
+    if world == 1:
+        return [t.tolist()]
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [o.tolist() for o in out]
+
+
+def scale_record(per_rank, bytes_per_step_per_rank: int, steps: int):
+    """Whole-job numbers from per-rank (elapsed_s, link_gbs): aggregate GB/s over the max elapsed time
+    (weak scaling: every rank moves its own bytes), and each rank's fraction of ITS OWN link ceiling,
+    measured while every rank ran its ceiling copy at once (the target holds per GPU)."""
+    elapsed = [r[0] for r in per_rank]
+    world = len(per_rank)
+    agg = bytes_per_step_per_rank * world * steps / max(elapsed) / 1e9
+    fracs = [bytes_per_step_per_rank * steps / r[0] / 1e9 / r[1] for r in per_rank]
+    return {"value": agg, "per_rank_gbs": [round(bytes_per_step_per_rank * steps / e / 1e9, 3) for e in elapsed],
+            "per_rank_link_gbs": [round(r[1], 3) for r in per_rank],
+            "per_rank_frac_of_link": [round(f, 4) for f in fracs], "min_frac_over_ranks": round(min(fracs), 4)}
+
+
+# ------------------------------------------------------------------------------------------------
 def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 10.0):
-    """The oracle as it stands (oracle/oracle.c, OpenMP over all host cores), timed on this box on the
-    same workload: DRAM->DRAM into host images of the device pool (SURVEY.md §8d "Oracle timing")."""
+    """The oracle as it stands (oracle/oracle.c, OpenMP over the cores this process may use), timed on
+    this box on the same workload: DRAM->DRAM into host images of the device pool (SURVEY §8d "Oracle
+    timing"); plus a single-threaded sample (layers of one load)."""
     import oracle
+    from paper_2508_18572_b200 import numa
     oracle.build()
     nb = g.num_pages * g.P * g.token_bytes
     k = [np.empty(nb, np.uint8) for _ in range(g.L)]
@@ -164,10 +208,24 @@ def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 10.0):
         oracle.load(g, host, k, v, q, 0, g.L, nthreads=threads)
         times.append(time.perf_counter() - t0)
     best = statistics.median(times)
+    # single thread: the first layers of one load, ~2 s
+    t0 = time.perf_counter()
+    nl = 0
+    while nl < g.L and (nl < 2 or time.perf_counter() - t0 < 2.0):
+        oracle.load(g, host, k, v, q, nl, nl + 1, nthreads=1)
+        nl += 1
+    one = time.perf_counter() - t0
+    node = numa.gpu_numa_node(0)
+    node_cpus = numa.parse_cpulist(open(f"/sys/devices/system/node/node{node}/cpulist").read()) \
+        if node >= 0 and os.path.exists(f"/sys/devices/system/node/node{node}/cpulist") else []
     return {"value": round(bytes_per / best / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "oracle",
             "sample": f"full {q.total_tokens}-token {g.L}-layer load of the bench workload, "
                       f"{len(times)} reps, median; DRAM->DRAM, {threads} OpenMP threads",
-            "ms_per_load": round(best * 1e3, 2)}
+            "ms_per_load": round(best * 1e3, 2),
+            "single_thread": {"value": round(bytes_per / g.L * nl / one / 1e9, 3), "unit": "GB/s", "cores": 1,
+                              "sample": f"{nl} layers of one load"},
+            "nproc": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0)), "gpu_numa_node": node,
+            "numa_node_cpus": len(node_cpus) or None}
 
 
 def run_reference(args):
@@ -208,20 +266,23 @@ def _config(args, g, q):
             "kv_buffers_per_layer": g.kv, "host_heads": g.host_heads, "head_begin": g.h0,
             "host_layout": "head-major" if g.head_major else "token-major",
             "page_size": g.P, "host_chunk_tokens": g.C, "tokens_per_gpu": q.total_tokens,
-            "requests": q.R, "fragmentation": args.frag, "host_chunk_order": args.chunk_frag, "bytes_per_step_per_gpu": g.kv * g.L * q.total_tokens * g.token_bytes,
+            "requests": q.R, "fragmentation": args.frag, "host_chunk_order": args.chunk_frag,
+            "bytes_per_step_per_gpu": g.kv * g.L * q.total_tokens * g.token_bytes,
             "l2": f"no flush: each step moves {g.kv * g.L * q.total_tokens * g.token_bytes / 2**30:.1f} GiB, "
-                  "far above the 126 MB L2", "parallelism": (f"tp{args.gpus}: KV-head slices of one host tier" if g.host_heads > g.H
+                  "far above the 126 MB L2",
+            "parallelism": (f"tp{args.gpus}: KV-head slices of one host tier" if g.host_heads > g.H
                             else f"replicas x{args.gpus}")}
 
 
-def main():
-    args = parse()
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         return run_reference(args)
     import torch
     import torch.distributed as dist
 
     import paper_2508_18572_b200 as st
+    from paper_2508_18572_b200 import numa
 
     rank, world, local = dist_env()
     # STRATA_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 with gloo for the barrier and
@@ -231,6 +292,7 @@ def main():
     if share:
         local = 0
     torch.cuda.set_device(local)
+    placement = numa.bind_to_gpu(local)
     red_dev = "cpu" if share else "cuda"
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -243,8 +305,9 @@ def main():
     nb = g.num_pages * g.P * g.token_bytes
     k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
     v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)] if g.kv == 2 else k
-    # A tier holding every KV head (R28) is ONE file-backed mapping shared by the ranks when the
-    # node's /dev/shm can hold it (rank 0 creates and fills it); otherwise each rank keeps a copy.
+    # A tier holding every KV head (R28) is one file-backed mapping per NUMA node, shared by the ranks
+    # on that node when its /dev/shm can hold it (the node's lowest rank creates, binds and fills it);
+    # otherwise each rank keeps a copy.
     shared, host_tier = None, "per-rank"
     if g.host_heads > g.H and world > 1:
         from paper_2508_18572_b200.shared_tier import SharedTier, free_bytes
@@ -252,14 +315,18 @@ def main():
         flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=red_dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()):
-            path = f"/dev/shm/strata_bench_tier_{os.environ.get('MASTER_PORT', '0')}"
-            if rank == 0:
+            nodes = gather_floats(dist, world, [placement["numa_node"]], device=red_dev)
+            node = placement["numa_node"]
+            creator = min(r for r in range(world) if int(nodes[r][0]) == node)
+            path = f"/dev/shm/strata_bench_tier_{os.environ.get('MASTER_PORT', '0')}_n{node}"
+            if rank == creator:
                 shared = SharedTier(path, g.host_bytes, create=True)
+                numa.mbind(shared.array.ctypes.data, g.host_bytes, node)
                 kvgen.fill_random(shared.array, args.seed * 1000)
             dist.barrier()
-            if rank != 0:
+            if rank != creator:
                 shared = SharedTier(path, g.host_bytes, create=False)
-            host_tier = f"one shared mapping for {world} ranks"
+            host_tier = f"one shared mapping per NUMA node ({len({int(n[0]) for n in nodes})} for {world} ranks)"
     pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
                        k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=g.num_pages,
                        num_chunks=g.num_chunks, device=local, host_heads=g.Ht, head_begin=g.h0,
@@ -279,72 +346,67 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def timed(fn, n):
+        """n back-to-back calls on `io`: (seconds, per-call ms) from CUDA events on the I/O stream."""
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        marks[0].record(io)
+        for i in range(n):
+            fn()
+            marks[i + 1].record(io)
+        marks[-1].synchronize()
+        per = [marks[i].elapsed_time(marks[i + 1]) for i in range(n)]
+        return marks[0].elapsed_time(marks[-1]) / 1e3, per
+
+    # host-link ceilings of THIS rank while every rank runs its own at once (barrier-aligned):
+    # contiguous pinned cudaMemcpyAsync of one layer's bytes from / to the same registered tier
+    scratch = torch.empty(bytes_step // g.L, dtype=torch.uint8, device="cuda")
+
+    def ceiling(direction):
+        barrier()
+        def cp():
+            st.strata_baseline_contiguous(pool.handle, direction, scratch.data_ptr(), 0, scratch.numel(), io)
+        cp()
+        _, per = timed(cp, 12)
+        return scratch.numel() / (statistics.median(per[2:]) / 1e3) / 1e9
+    link_h2d = ceiling(st.STRATA_H2D)
+    link_d2h = ceiling(st.STRATA_D2H)
+
     for _ in range(args.warmup):
         step()
+
     def timed_region():
         barrier()
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         c0 = pool.counters()
         with ClockSampler(local) as clocks:
-            start.record(io)
-            last = None
-            host_s = 0.0   # CPU time inside the strata_load calls (submission; blocks only when queued ahead)
-            for i in range(args.steps):
-                marks[i].record(io)
-                h0 = time.perf_counter()
-                last = step()
-                host_s += time.perf_counter() - h0
-            marks[-1].record(io)
-            end.record(io)
+            h0 = time.perf_counter()
+            elapsed, step_ms = timed(step, args.steps)
+            host_s = time.perf_counter() - h0
+            last = pool.counters()
             barrier()
-        c1 = pool.counters()
-        step_ms = sorted(marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps))
-        return (start.elapsed_time(end) / 1e3, step_ms, host_s, last, clocks,
-                c1["kernel_launches"] - c0["kernel_launches"], c1)
+        return elapsed, sorted(step_ms), host_s, clocks, last["kernel_launches"] - c0["kernel_launches"], last
 
-    elapsed, step_ms, host_s, last, clocks, launches, c1 = timed_region()
+    elapsed, step_ms, host_s, clocks, launches, c1 = timed_region()
     # A timed region whose steps vary by more than 5 % (CV) saw something outside this process —
     # e.g. the host still reclaiming memory a previous job freed, which slows the link itself — and is
     # re-measured once (SURVEY §8d); the first measurement is kept in the line.
     cv = statistics.pstdev(step_ms) / statistics.mean(step_ms)
-    tcv = torch.tensor([cv], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(tcv, op=dist.ReduceOp.MAX)
     remeasured = None
-    if float(tcv.item()) > 0.05:
-        remeasured = {"first_elapsed_s": round(elapsed, 4), "first_cv_max_over_ranks": round(float(tcv.item()), 4)}
+    if reduce_max(dist, world, cv, red_dev) > 0.05:
+        remeasured = {"first_elapsed_s": round(elapsed, 4), "first_cv_max_over_ranks": round(cv, 4)}
         time.sleep(2.0)
-        elapsed, step_ms, host_s, last, clocks, launches, c1 = timed_region()
+        elapsed, step_ms, host_s, clocks, launches, c1 = timed_region()
     engine_used = ENGINE_NAMES.get(c1["last_engine"], str(c1["last_engine"]))
     step_stats = {"median_ms": round(statistics.median(step_ms), 3),
                   "p10_ms": round(step_ms[int(0.1 * (len(step_ms) - 1))], 3),
                   "p90_ms": round(step_ms[int(0.9 * (len(step_ms) - 1))], 3),
                   "min_ms": round(step_ms[0], 3), "max_ms": round(step_ms[-1], 3),
                   "cv": round(statistics.pstdev(step_ms) / statistics.mean(step_ms), 4)}
-    # per-layer (= per-launch) durations of the last timed step, from the library's own events
-    t_layer = [pool.layer_elapsed_ms(last, l) for l in range(g.L)]
-    launch_ms = [t_layer[0]] + [b - a for a, b in zip(t_layer, t_layer[1:])]
-    t = torch.tensor([elapsed], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_max = float(t.item())
-    value = bytes_step * world * args.steps / elapsed_max / 1e9
-
-    # link roofline: one contiguous cudaMemcpyAsync of the same bytes-per-layer from the same host tier
-    scratch = torch.empty(bytes_step // g.L, dtype=torch.uint8, device="cuda")
-    rt = []
-    for i in range(13):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(io)
-        for _l in range(4):
-            st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, scratch.numel(), io)
-        b.record(io)
-        b.synchronize()
-        if i >= 3:
-            rt.append(4 * scratch.numel() / (a.elapsed_time(b) / 1e3) / 1e9)
-    link_peak = statistics.median(rt)
-    del scratch
+    # per-layer completion times of the last timed step, from the library's own events
+    t_layer = [pool.layer_elapsed_ms(0, l) for l in range(g.L)]   # ticket 0: the latest operation
+    layer_ms = [t_layer[0]] + [b - a for a, b in zip(t_layer, t_layer[1:])]
+    per_rank = gather_floats(dist, world, [elapsed, link_h2d], red_dev)
+    rec = scale_record(per_rank, bytes_step, args.steps)
+    elapsed_max = max(r[0] for r in per_rank)
 
     # e2e through the public API with host buffers: upload the step's tables from pinned host
     # memory, load (the KV itself crosses host->device inside), read back the last loaded row.
@@ -361,51 +423,75 @@ def main():
             reqs.dev_pages_d.copy_(dp_pin, non_blocking=True)
         step()
         with torch.cuda.stream(io):
-            sentinel.copy_(v[g.L - 1][last_page * g.P * g.token_bytes: last_page * g.P * g.token_bytes + 16],
-                           non_blocking=True)
+            off = last_page * g.P * g.token_bytes
+            sentinel.copy_(v[g.L - 1][off: off + 16], non_blocking=True)
         io.synchronize()
-    e2e_dt = time.perf_counter() - t0
-    te = torch.tensor([e2e_dt], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = bytes_step * world * e2e_steps / float(te.item()) / 1e9
+    e2e_dt = reduce_max(dist, world, time.perf_counter() - t0, red_dev)
+    e2e_value = bytes_step * world * e2e_steps / e2e_dt / 1e9
     h2d = bytes_step + 4 * (reqs.host_chunks_h.size + reqs.dev_pages_h.size)
 
-    # the other engines on the same workload, default SM quota, for comparison in the same line
-    others = {}
-    for eng in (st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_DMA):
-        if ENGINE_NAMES[eng] == engine_used:
-            continue
-        pool.load(reqs, 0, g.L, stream=io, engine=eng)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(io)
-        for _ in range(3):
-            pool.load(reqs, 0, g.L, stream=io, engine=eng)
-        b.record(io)
-        b.synchronize()
-        others[ENGINE_NAMES[eng]] = round(3 * bytes_step / (a.elapsed_time(b) / 1e3) / 1e9, 3)
+    extras = {}
+    if not args.no_extras:
+        n_x = max(3, min(args.steps, 10))
+        # the same workload at page size 16 (the target holds at P = 1 and 16): a second
+        # pool over the same device buffers and host tier, P=16 page tables
+        g16, q16 = workload(args, rank, world, P=16)
+        assert g16.num_pages * 16 <= g.num_pages * g.P, "P=16 pool must fit the device buffers"
+        pool16 = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=16,
+                             chunk_tokens=g.C, k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=g16.num_pages,
+                             num_chunks=g.num_chunks, device=local, host_heads=g.Ht, head_begin=g.h0,
+                             head_major=g.head_major, host=pool.host)
+        reqs16 = st.Requests.from_kvgen(q16, device=local)
+        f16 = lambda: pool16.load(reqs16, 0, g.L, stream=io, engine=args.engine, num_ctas=args.num_ctas)  # noqa: E731
+        f16()
+        barrier()
+        e16, _ = timed(f16, n_x)
+        pr16 = scale_record(gather_floats(dist, world, [e16, link_h2d], red_dev), bytes_step, n_x)
+        extras["page_size_16"] = {"value": round(pr16["value"], 3), "frac_of_link": pr16["min_frac_over_ranks"],
+                                  "steps": n_x, "engine": ENGINE_NAMES.get(pool16.counters()["last_engine"])}
+        pool16.close()
+        # offload (write-back) of the same workload at its default quota vs the D2H link
+        fo = lambda: pool.offload(reqs, 0, g.L, stream=io)  # noqa: E731
+        fo()
+        barrier()
+        eo, _ = timed(fo, n_x)
+        pro = scale_record(gather_floats(dist, world, [eo, link_d2h], red_dev), bytes_step, n_x)
+        extras["offload"] = {"value": round(pro["value"], 3), "frac_of_d2h_link": pro["min_frac_over_ranks"],
+                             "d2h_link_gbs": round(link_d2h, 3), "steps": n_x,
+                             "engine": ENGINE_NAMES.get(pool.counters()["last_engine"]), "num_ctas": "default"}
+        # zero-copy contiguous ceiling (diagnostic): the same kernel and quota on consecutive
+        # host chunks and consecutive pages — what the SM zero-copy path reaches with no fragmentation
+        qi = kvgen.make_requests(kvgen.rng_for(0), kvgen.CONFIGS[args.config]["n"], g.P, g.C, g.num_pages,
+                                 g.num_chunks, frag="identity", chunk_frag="identity")
+        reqs_i = st.Requests.from_kvgen(qi, device=local)
+        fi = lambda: pool.load(reqs_i, 0, g.L, stream=io, engine=args.engine, num_ctas=args.num_ctas)  # noqa: E731
+        fi()
+        ei, _ = timed(fi, 3)
+        extras["zero_copy_contiguous_gbs"] = round(bytes_step * 3 / ei / 1e9, 3)
+        # the other engines on the same workload at their default quotas (3 loads each)
+        others = {}
+        for eng in (st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_DMA):
+            if ENGINE_NAMES[eng] == engine_used:
+                continue
+            fe = lambda: pool.load(reqs, 0, g.L, stream=io, engine=eng)  # noqa: E731
+            fe()
+            ee, _ = timed(fe, 3)
+            others[ENGINE_NAMES[eng]] = round(bytes_step * 3 / ee / 1e9, 3)
+        extras["other_engines_gbs"] = others
+    del scratch
 
     out = None
     if rank == 0:
-        # per layer (= per launch for the kernel engines; per copy+scatter group for DMA): the median
-        # timed step divided over its layers, from CUDA events on the I/O stream
-        per_launch_bytes = bytes_step // g.L
-        avg_launch = step_stats["median_ms"] / g.L
+        # the dominant kernel: one launch per step for the fused engines (ring / LDG), so its average
+        # launch duration is the median step; per layer for DMA
+        launches_per_step = max(1, launches // args.steps)
+        per_launch_bytes = bytes_step // launches_per_step
+        avg_launch = step_stats["median_ms"] / launches_per_step
         achieved = per_launch_bytes / (avg_launch / 1e3) / 1e9
-        # the hand-written zero-copy kernels against both ceilings: the link, and the SM-issued
-        # zero-copy read plateau measured by tools/probe/probe.cu on this pool (51.44 GB/s)
-        zc = {}
-        for name in ("ldg", "tma"):
-            gbs = others.get(name) if name != engine_used else round(value / world, 3)
-            if gbs is not None:
-                zc[name] = {"value": gbs, "frac_of_link": round(gbs / link_peak, 4),
-                            "frac_of_sm_zero_copy_ceiling": round(gbs / SM_ZERO_COPY_CEILING, 4),
-                            "num_ctas": "default (2 x 1024 threads)" if name == "ldg" else "default (2 x 512 threads)"}
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(f"{args.config}_P{g.P}_{engine_used}")
-        path = PATH_DESC.get(engine_used, engine_used)
         peaks = {}
         mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
         if os.path.exists(mp):
@@ -414,21 +500,25 @@ def main():
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(g, q, pool.host)
-        batches = -(-q.R // 128)
         out = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": round(rec["value"], 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(elapsed_max / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": _config(args, g, q),
             "ms_per_32k_load": round(elapsed_max / args.steps * 1e3 * 32768 / q.total_tokens, 3),
+            "engine": engine_used, "num_ctas": args.num_ctas or "default",
             "step_stats_rank0": step_stats,
-            "frac_of_link": round(value / world / link_peak, 4),
-            "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3), "peak": round(link_peak, 3),
-                         "unit": "GB/s", "frac": round(achieved / link_peak, 4), "traffic": traffic,
-                         "kernel": path,
+            "frac_of_link": rec["min_frac_over_ranks"],
+            "per_rank": {k_: rec[k_] for k_ in ("per_rank_gbs", "per_rank_link_gbs", "per_rank_frac_of_link",
+                                                "min_frac_over_ranks")},
+            "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3), "peak": round(link_h2d, 3),
+                         "unit": "GB/s", "frac": round(achieved / link_h2d, 4), "traffic": traffic,
+                         "kernel": PATH_DESC.get(engine_used, engine_used),
                          "per_launch_bytes": per_launch_bytes, "avg_launch_ms": round(avg_launch, 4),
+                         "launches_per_step": launches_per_step,
                          "peak_source": "contiguous pinned cudaMemcpyAsync H2D from the same registered host "
-                                        "tier, measured in this run (PCIe Gen5 x16 nominal 64 GB/s)",
+                                        "tier, measured in this run on this rank (concurrently with every other "
+                                        "rank); PCIe Gen5 x16 nominal 64 GB/s",
                          "hbm": {"achieved": round(achieved, 3), "peak": hbm_peak,
                                  "frac": round(achieved / hbm_peak, 5),
                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}},
@@ -437,13 +527,11 @@ def main():
                     "d2h_bytes_per_step": 16},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
-            "engine": engine_used, "num_ctas": args.num_ctas or "default",
-            "layer_group": args.layer_group or "default",
-            "other_engines_gbs": others,
+            "placement": placement,
+            **extras,
             "shared_gpu_test_mode": share or None,
             "host_tier": host_tier,
-            "zero_copy_kernels": zc,
-            "per_layer_ms_last_step": [round(x, 4) for x in launch_ms],
+            "per_layer_ms_last_step": [round(x, 4) for x in layer_ms],
             "host_submit_ms_per_step": round(host_s / args.steps * 1e3, 3),
             "remeasured": remeasured,
         }

@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cpp", "transfer.cpp", "dma.cpp", "kernels.cu", "baselines.cpp", "disk.cpp", "ctl.cpp"]
+SOURCES = ["api.cpp", "transfer.cpp", "dma.cpp", "kernels.cu", "ring.cu", "baselines.cpp", "disk.cpp", "ctl.cpp"]
 OUT = os.path.join(HERE, "libstrata.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
@@ -47,6 +48,7 @@ int strata::fail(int code, const char* fmt, ...) {
 }
 
 int strata::cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();   // the failing call just set it: leave no stale error for the caller's next launch
   return fail(STRATA_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
@@ -154,8 +156,60 @@ int check_desc(const strata_pool_desc* d) {
   return STRATA_OK;
 }
 
+// Caller memory registered by this library, shared by every pool whose tier lies inside it (e.g. one
+// host tier holding every KV head, read by the pools of several TP ranks, R28): the registration is
+// undone only when the last of those pools closes, never while another still reads it through UVA.
+struct HostReg {
+  char* base;
+  size_t bytes;
+  int refs;
+};
+std::mutex g_reg_mu;
+std::vector<HostReg> g_regs;
+
+// 0: registered (or shared) by the library, 1: registered by someone else (not ours to undo).
+cudaError_t register_caller(char* base, size_t bytes, bool& ours) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  for (auto& r : g_regs)
+    if (base >= r.base && base + bytes <= r.base + r.bytes) {
+      ++r.refs;
+      ours = true;
+      return cudaSuccess;
+    }
+  cudaError_t e = cudaHostRegister(base, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    ours = false;
+    return cudaSuccess;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
+  }
+  g_regs.push_back({base, bytes, 1});
+  ours = true;
+  return cudaSuccess;
+}
+
+void unregister_caller(char* base, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  for (size_t i = 0; i < g_regs.size(); ++i) {
+    HostReg& r = g_regs[i];
+    if (base >= r.base && base + bytes <= r.base + r.bytes) {
+      if (--r.refs == 0) {
+        cudaHostUnregister(r.base);
+        g_regs.erase(g_regs.begin() + static_cast<std::ptrdiff_t>(i));
+      }
+      return;
+    }
+  }
+}
+
 void free_host(strata_pool* p) {
-  if (p->registered_by_us && p->host) cudaHostUnregister(p->host);
+  if (p->registered_by_us && p->host) {
+    if (p->host_kind == 0) unregister_caller(p->host, p->host_bytes);
+    else cudaHostUnregister(p->host);
+  }
   if (p->host_kind == 1 && p->host) munmap(p->host, p->map_bytes);
   if (p->host_kind == 2 && p->host) cudaFreeHost(p->host);
   p->host = nullptr;
@@ -242,16 +296,14 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
   if (d->host_base) {
     p->host = static_cast<char*>(d->host_base);
     p->host_kind = 0;
-    e = cudaHostRegister(p->host, p->host_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
-    if (e == cudaErrorHostMemoryAlreadyRegistered) {
-      cudaGetLastError();
-    } else if (e != cudaSuccess) {
+    bool ours = false;
+    e = register_caller(p->host, p->host_bytes, ours);
+    if (e != cudaSuccess) {
       p->host = nullptr;
       delete p;
       return cuda_fail(e, "cudaHostRegister(host_base)");
-    } else {
-      p->registered_by_us = true;
     }
+    p->registered_by_us = ours;
   } else if (d->flags & (STRATA_HOST_WRITECOMBINED | STRATA_HOST_CUDA_ALLOC)) {
     void* h = nullptr;
     unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
@@ -306,7 +358,7 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
   }
   for (auto& op : p->ops) op = {0, 0, 0};
   p->tma_smem = strata::tma_smem_limit();
-  if (p->tma_smem > 0 && (e = strata::tma_prepare(p->tma_smem))) {
+  if (p->tma_smem > 0 && ((e = strata::tma_prepare(p->tma_smem)) || (e = strata::ring_prepare(p->tma_smem)))) {
     destroy(p);
     return cuda_fail(e, "cudaFuncSetAttribute(TMA smem)");
   }
@@ -320,7 +372,7 @@ int strata_unregister_host_pool(strata_pool_t p) {
   DeviceGuard dg(p->d.device);
   // wait for every operation whose events are still live
   for (const auto& op : p->ops) {
-    if (op.ticket && op.l1 > op.l0) {
+    if (op.ticket && op.l1 > op.l0 && !op.captured) {
       const int slot = static_cast<int>(op.ticket % kEventRing);
       cudaEventSynchronize(p->events[size_t(slot) * (p->d.num_layers + 1) + op.l1]);
     }
@@ -398,6 +450,9 @@ int strata_layer_elapsed_ms(strata_pool_t p, uint64_t ticket, int32_t layer, flo
   int slot = 0;
   int rc = find_op(p, ticket, layer, slot);
   if (rc) return rc;
+  if (p->ops[slot].captured)
+    return fail(STRATA_ERR_UNSUPPORTED, "ticket %llu was captured into a CUDA graph: its events exist only inside "
+                "that graph (time the graph's replay instead)", (unsigned long long)ticket);
   const size_t base = size_t(slot) * (p->d.num_layers + 1);
   cudaError_t e = cudaEventSynchronize(p->events[base + 1 + layer]);
   if (e == cudaSuccess) e = cudaEventElapsedTime(ms, p->events[base], p->events[base + 1 + layer]);

@@ -40,9 +40,18 @@ constexpr size_t kStageTarget = size_t(128) << 20;
 constexpr int kDefaultCtasScatter = 8;
 constexpr size_t kDmaMinEdgePiece = size_t(16) << 20;   // edge pieces are not cut below this
 
-static int ensure_dma(strata_pool* p, strata_pool::DmaDir& D, size_t slot_bytes, int64_t slots) {
+// Staging buffers are allocated once, at the first DMA operation of a direction, at their full size
+// (the stage target, or one group of chunk-layers if that is larger) so that they never move: a CUDA
+// graph that captured a DMA operation keeps pointing at them.  A later operation that would need
+// more (only with STRATA_STAGE_MB raised, or a group larger than the target) is refused once this
+// direction has been captured, and reallocates otherwise.
+static int ensure_dma(strata_pool* p, strata_pool::DmaDir& D, size_t slot_bytes, int64_t slots, size_t full_bytes,
+                      int64_t full_slots, bool capturing) {
   cudaError_t e;
+  if (capturing) D.captured = true;
   if (!D.cs[0]) {
+    if (capturing) return fail(STRATA_ERR_UNSUPPORTED, "the first STRATA_ENGINE_DMA operation of a pool and "
+                                                       "direction must run outside stream capture (it allocates)");
     if (const char* v = getenv("STRATA_COPY_STREAMS"))
       D.ncs = std::max(1, std::min(strata_pool::kCopyStreams, atoi(v)));
     for (auto& c : D.cs)
@@ -54,27 +63,36 @@ static int ensure_dma(strata_pool* p, strata_pool::DmaDir& D, size_t slot_bytes,
         if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
     }
   }
+  const bool grow_stage = D.stage_bytes < slot_bytes, grow_ids = p->slot_cap < slots;
+  if (grow_stage || grow_ids) {
+    if ((grow_stage && D.captured) || (grow_ids && (p->dma[0].captured || p->dma[1].captured)))
+      return fail(STRATA_ERR_UNSUPPORTED, "STRATA_ENGINE_DMA staging would have to grow (%zu -> %zu bytes) after a "
+                  "graph captured it", D.stage_bytes, slot_bytes);
+    cudaDeviceSynchronize();   // earlier operations may still use the old buffers
+  }
   if (D.stage_bytes < slot_bytes) {
     for (auto& b : D.stage) {
       if (b) cudaFree(b);
       b = nullptr;
     }
     D.stage_bytes = 0;
+    const size_t want = std::max(slot_bytes, full_bytes);
     for (auto& b : D.stage)
-      if ((e = cudaMalloc(&b, slot_bytes))) return fail(STRATA_ERR_OOM, "cudaMalloc(staging %zu): %s", slot_bytes,
-                                                        cudaGetErrorString(e));
-    D.stage_bytes = slot_bytes;
+      if ((e = cudaMalloc(&b, want))) return fail(STRATA_ERR_OOM, "cudaMalloc(staging %zu): %s", want,
+                                                  cudaGetErrorString(e));
+    D.stage_bytes = want;
   }
   if (p->slot_cap < slots) {
     if (p->slot_ids) cudaFree(p->slot_ids);
     p->slot_ids = nullptr;
     p->slot_cap = 0;
-    std::vector<int32_t> iota(static_cast<size_t>(slots));
-    for (int64_t i = 0; i < slots; ++i) iota[i] = static_cast<int32_t>(i);
+    const int64_t n = std::max(slots, full_slots);
+    std::vector<int32_t> iota(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) iota[i] = static_cast<int32_t>(i);
     if ((e = cudaMalloc(&p->slot_ids, iota.size() * 4))) return cuda_fail(e, "cudaMalloc(slot ids)");
     if ((e = cudaMemcpy(p->slot_ids, iota.data(), iota.size() * 4, cudaMemcpyHostToDevice)))
       return cuda_fail(e, "cudaMemcpy(slot ids)");
-    p->slot_cap = slots;
+    p->slot_cap = n;
   }
   return STRATA_OK;
 }
@@ -353,7 +371,12 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   const size_t edge_cap = std::min(per_piece, std::max<size_t>({1, per_piece / size_t(edge), kDmaMinEdgePiece / m.gunit}));
   const std::vector<Piece> edge_pieces = edge_cap < per_piece ? make_pieces(pos, edge_cap) : pieces;
   strata_pool::DmaDir& D = p->dma[dir];
-  rc = ensure_dma(p, D, per_piece * m.gunit, static_cast<int64_t>(per_piece));
+  cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &capst) != cudaSuccess) return cuda_fail(cudaErrorUnknown, "cudaStreamIsCapturing");
+  // full size: the stage target over the smallest run unit (one chunk-layer), at least this call's
+  rc = ensure_dma(p, D, per_piece * m.gunit, static_cast<int64_t>(per_piece), stage_target,
+                  static_cast<int64_t>(std::max<size_t>(1, stage_target / m.unit)),
+                  capst == cudaStreamCaptureStatusActive);
   if (rc) return rc;
 
   cudaError_t e;
@@ -376,8 +399,6 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   int64_t i = 0;                 // pieces of this operation
   // pieces of this direction, across operations; a graph capture starts its own sequence (its
   // nodes may not depend on uncaptured work, and a replay is ordered by the graph's own edges)
-  cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
-  if ((e = cudaStreamIsCapturing(s, &capst))) return cuda_fail(e, "cudaStreamIsCapturing");
   uint64_t capture_seq = 0;
   uint64_t& seq = capst == cudaStreamCaptureStatusActive ? capture_seq : D.seq;
   int last_slot = 0;

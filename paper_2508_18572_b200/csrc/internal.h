@@ -93,11 +93,45 @@ struct FusedParams {
   char* vb[kMaxFusedLayers];
 };
 
+// The ring engine (ring.cu, STRATA_ENGINE_TMA): a persistent kernel over every layer of an operation
+// whose unit of work is a PIECE — up to `rows` consecutive tokens of one (request, host chunk, K|V)
+// segment, i.e. one contiguous run of the page-first host chunk.  A piece crosses
+// the host link as ONE cp.async.bulk (TMA) through a `stages`-deep shared-memory ring; its rows are
+// scattered to / gathered from their pages on the device side.
+//   piece k of a layer: segment k / pps, sub-piece k % pps; segment -> (pair = chunk position of a
+//   request, kv); pair -> request by binary search over pair_end.
+constexpr int kRingMaxStages = 16;
+constexpr int kRingMaxWarps = 16;   // LSU scatter warps of a load CTA
+constexpr int kRingMaxRows = 128;   // rows per piece
+struct RingParams {
+  XferParams x;                 // geometry, index lists, request table (kbase/vbase/layer_off unused)
+  int32_t l0, l1;               // layer range
+  uint32_t epoch;               // published to flags[l] when layer l is complete
+  int32_t arrivals;             // arrivals per layer: load = CTAs * warps, offload = CTAs
+  uint32_t* counters;           // [L] arrival counters of the op slot, or NULL: no per-layer flags
+  uint32_t* flags;              // [L] completion flags of the op slot
+  int32_t rows;                 // R: rows per piece (<= kRingMaxRows, <= 32 * warps)
+  int32_t stages;               // S: ring depth (<= kRingMaxStages)
+  int32_t stage_bytes;          // bytes per stage (R * tok rounded up to 128)
+  int32_t pps;                  // pieces per segment = ceil(C / R)
+  int32_t npieces;              // pieces per layer
+  int32_t host_run;             // 1: a piece's host rows are one contiguous run (host_tok_stride == tok)
+  int32_t warps;                // device-side LSU warps per CTA: load scatter / offload gather (+1 TMA warp)
+  uint32_t piece_magic;         // row of vector v < R*vpt: umulhi(v, magic) (0: vpt_shift or divide)
+  int32_t pair_end[kMaxReqsPerLaunch];   // inclusive prefix sums of chunk positions per request
+  char* kb[kMaxFusedLayers];    // per-layer K / V bases
+  char* vb[kMaxFusedLayers];
+};
+// Shared-memory bytes in front of the ring's stages (mbarriers + per-stage row-address tables).
+int ring_header_bytes(int stages, int rows);
+cudaError_t launch_ring(const RingParams& p, int dir, int ctas, cudaStream_t s);
+cudaError_t ring_prepare(int smem);
+
 // Kernel launchers (kernels.cu).  dir: 0 = load (host -> device), 1 = offload (device -> host).
 cudaError_t launch_ldg(const XferParams& p, int dir, int ctas, int threads, int unroll, cudaStream_t s);
 cudaError_t launch_ldg_fused(const FusedParams& p, int dir, int ctas, int threads, cudaStream_t s);
-// warp_specialized (load only): 1 TMA producer warp + LSU consumer warps; else one bulk-only warp.
-cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s);
+// STRATA_ENGINE_TMA_BULK: one warp per CTA, cp.async.bulk on both sides of a shared-memory ring.
+cudaError_t launch_tma(const XferParams& p, int dir, int ctas, cudaStream_t s);
 cudaError_t launch_validate(const ValidateParams& v, cudaStream_t s);
 // Largest dynamic shared memory the TMA engine may use per CTA on this device.
 int tma_smem_limit();
@@ -134,7 +168,8 @@ struct strata_pool {
   // per-layer completion events: ring of kEventRing operations x L layers
   std::vector<cudaEvent_t> events;
   // fused: the op ran as one fused LDG launch; its layer l is complete once flags[slot][l] >= epoch
-  struct Op { uint64_t ticket; int32_t l0, l1; bool fused = false; };
+  // captured: recorded into a CUDA graph capture; its events exist only inside that graph
+  struct Op { uint64_t ticket; int32_t l0, l1; bool fused = false; bool captured = false; };
   Op ops[strata::kEventRing];
   uint64_t next_ticket = 1;
   // validate scratch (device)
@@ -162,6 +197,7 @@ struct strata_pool {
     cudaEvent_t ev_slot[2] = {nullptr, nullptr};   // staging slot reusable
     cudaEvent_t ev_copy[2][kCopyStreams] = {};     // a slot's copies done, per stream
     uint64_t seq = 0;                 // pieces issued in this direction so far
+    bool captured = false;            // a graph captured this direction: its buffers must not move
   } dma[2];
   int32_t* slot_ids = nullptr;        // device iota [0, slot_cap): chunk index of each staging slot
   int64_t slot_cap = 0;
@@ -224,7 +260,14 @@ constexpr int64_t kDmaMinLayerBytes = int64_t(4) << 20;
 constexpr int64_t kDmaMinOffloadRun = int64_t(128) << 10;
 constexpr int64_t kDmaMinLoadRun = int64_t(24) << 10;   // default engine: DMA loads need >= 24 KiB runs
 constexpr int kDefaultUnroll = 8;
-constexpr int kDefaultCtasTma = 2;   // warp-specialised ring: 51.0 GB/s at 2 CTAs (sweep_tma_ws15.jsonl)
+constexpr int kDefaultCtasTma = 2;   // STRATA_ENGINE_TMA_BULK (scaled up for small rows, transfer.cpp)
+// The ring engine (ring.cu), the default.  Loads: CTAs of 1 producer + kDefaultRingWarps scatter
+// warps; offloads: CTAs of 1 gather + 1 store warp; 32 KiB pieces, as many stages as fit.
+constexpr int kDefaultCtasRingLoad = 2;
+constexpr int kDefaultCtasRingOffload = 1;
+constexpr int kDefaultRingWarps = 8;         // load: scatter warps
+constexpr int kDefaultRingGatherWarps = 4;   // offload: cp.async gather warps
+constexpr int kDefaultRingStageKB = 32;
 constexpr int kTmaStageTarget = 32 << 10;
 
 int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan);                     // transfer.cpp

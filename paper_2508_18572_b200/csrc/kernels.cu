@@ -14,9 +14,8 @@
 //                       fetches row t's indices (one group ahead) and the warp streams the rows
 //                       with U independent 16-byte LDG/STG per lane, addresses broadcast by
 //                       __shfl_sync.  Also the scatter / gather of the DMA engine (HBM staging).
-//   tma_ws_load_kernel  zero-copy TMA: one producer warp issues one cp.async.bulk per contiguous
-//                       host run into a shared-memory ring; 15 consumer warps drain it to the pages.
-//   tma_kernel          zero-copy TMA, single warp, bulk copies on both sides of the ring.
+//   tma_kernel          zero-copy TMA, single warp, bulk copies on both sides of the ring
+//                       (STRATA_ENGINE_TMA_BULK).  The ring engine (STRATA_ENGINE_TMA) is ring.cu.
 //   ldg_fused_kernel    the LDG engine over every layer of an operation in one launch, per-layer
 //                       completion published as device flags.
 //   ldg_narrow_kernel   the LDG engine's shape over 8/4/2/1-byte words, for pools whose rows,
@@ -28,12 +27,13 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "device.cuh"
 #include "internal.h"
 
 namespace strata {
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
+using namespace dev;
 
 // ---------------------------------------------------------------------------------------------
 // Index fetch + layout transform for one token row.  Row = (kv, g): kv-major over the launch's
@@ -103,32 +103,10 @@ __device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x,
 }
 
 // ---------------------------------------------------------------------------------------------
-// 16-byte vector accesses.  Sources are read once: no L1 allocation.
-__device__ __forceinline__ int4 ld_stream(const void* ptr) {
-  int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr));
-  return r;
-}
-__device__ __forceinline__ void st_vec(void* ptr, const int4& v) {
-  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" :: "l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w) : "memory");
-}
-
-// ---------------------------------------------------------------------------------------------
 // LDG engine.  DIR 0: host -> device, DIR 1: device -> host.  CONTIG: device rows head-contiguous
 // (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
 // One layer of the LDG engine for this warp: groups warp, warp + nwarps, ...  `nx` holds the
 // already-fetched indices of the warp's first group (identical for every layer).
-// Address of 16-byte vector w of a row on one side: rows whose heads are adjacent are contiguous;
-// otherwise head h = w / vph sits at h * stride (device HND / padded heads, head-major host tiers).
-template <bool CONTIG>
-__device__ __forceinline__ uint64_t row_vec(uint64_t base, int w, const XferParams& p, int64_t stride) {
-  if (CONTIG) return base + static_cast<uint64_t>(w) * 16;
-  const int h = p.vph_shift >= 0 ? (w >> p.vph_shift) : (w / p.vph);
-  return base + h * stride + static_cast<uint64_t>(w - h * p.vph) * 16;
-}
-
 template <int U, bool CONTIG, bool HCONTIG, int DIR>
 __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char* vbase, int64_t layer_off,
                                           RowIdx nx, int64_t warp, int64_t nwarps, int lane) {
@@ -207,17 +185,6 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_kernel(const __gri
 // layer's CUDA event with cuStreamWaitValue32 + cudaEventRecord on the op slot's side stream.
 // Loads land in HBM and are consumed by GPU work: GPU-scope fences.  Offloads land in host memory,
 // which the host may read after the event: system scope.
-template <int DIR>
-__device__ __forceinline__ void layer_fence() {
-  if (DIR == 0) __threadfence();
-  else __threadfence_system();
-}
-template <int DIR>
-__device__ __forceinline__ void st_release(uint32_t* a, uint32_t v) {
-  if (DIR == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
-  else asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(a), "r"(v) : "memory");
-}
-
 template <int U, bool CONTIG, bool HCONTIG, int DIR>
 __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const __grid_constant__ FusedParams fp) {
   const XferParams& p = fp.x;
@@ -240,40 +207,6 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const
     }
   }
 }
-
-// ---------------------------------------------------------------------------------------------
-// TMA engine primitives (cp.async.bulk non-tensor copies + mbarrier transaction counts).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n}\n" :: "r"(smem_u32(b)), "r"(parity) : "memory");
-}
-// global (device or mapped host) -> shared, completes `bytes` on barrier `bar`
-__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               :: "r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-// shared -> global (device or mapped host), tracked by this thread's bulk async-groups
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-               :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 constexpr int kTmaHeader = 16 * kTmaMaxStages;           // mbarriers: full[32], empty[32]
 
@@ -299,7 +232,7 @@ __global__ void __launch_bounds__(32, 1) tma_kernel(const __grid_constant__ Xfer
 
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   __syncwarp();
 
@@ -386,127 +319,12 @@ __global__ void __launch_bounds__(32, 1) tma_kernel(const __grid_constant__ Xfer
     if (k >= 1 && k - 1 + S < my) {
       const RowIdx cur = nx;          // fetched one step ago: piece k-1+S
       nx = fetch(k + S);
-      bulk_wait_read1();
+      bulk_wait_read<1>();
       __syncwarp();
       issue(k - 1 + S, cur);
     }
   }
   bulk_wait_all();
-}
-
-// ---------------------------------------------------------------------------------------------
-// Warp-specialised TMA load (the default load engine).  Warp 0 is the producer: it fetches the
-// indices of a piece (software-pipelined one piece ahead), publishes each row's device address in a
-// per-stage table, and issues ONE cp.async.bulk per contiguous host run into the stage.  Warps
-// 1..kWsConsumers drain a full stage to the pages with ld.shared.v4 / st.global.v4 (16-byte
-// vectors, any page size or head stride) and release it on the stage's `empty` mbarrier.  The TMA
-// unit only sees large contiguous host reads; the scattered small writes go through the LSU, so one
-// SM sustains ~45 GB/s of host reads and two saturate the PCIe link (the paper's 2-CTA quota,
-// PAPER.md:262).
-// Each consumer warp drains ~7 GB/s of st.global.v4 (tools/probe/tma_probe.cu ring_ws: 1/2/4/8
-// consumer warps -> 7/14/25/40 GB/s from one SM), so one SM needs ~8+ consumers to match the link.
-constexpr int kWsConsumers = 15;
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ int4 ld_shared_v4(const void* p) {
-  int4 r;
-  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "r"(smem_u32(p)));
-  return r;
-}
-
-template <bool CONTIG>
-__global__ void __launch_bounds__(32 * (1 + kWsConsumers), 1) tma_ws_load_kernel(const __grid_constant__ XferParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int S = p.tma_stages;
-  const int T = p.tma_rows;
-  const int SB = p.tma_stage_bytes;
-  const int tok = p.tok_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kTmaMaxStages;
-  uint64_t* tab_addr = reinterpret_cast<uint64_t*>(smem + kTmaHeader);   // [S][32] device row address
-  unsigned char* buf = smem + tma_buf_offset(S);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  // Every producer lane arrives on `full` itself, so each lane's address-table write is released by
-  // its own arrive (with one arrive by lane 0 after __syncwarp, compute-sanitizer racecheck reported
-  // the table writes as racing with the consumers' reads); consumers arrive once per warp.
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], kWsConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
-  const int64_t npieces = (nrows + T - 1) / T;
-  const int64_t my = npieces > blockIdx.x ? (npieces - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-
-  if (warp == 0) {
-    // ---------------- producer ----------------
-    auto fetch = [&](int64_t k) {
-      const int64_t row = (blockIdx.x + k * gridDim.x) * T + lane;
-      return (k < my && lane < T && row < nrows) ? row_fetch(p, row) : row_none();
-    };
-    RowIdx nx = fetch(0);
-    for (int64_t k = 0; k < my; ++k) {
-      const int s = static_cast<int>(k % S);
-      const RowIdx cur = nx;
-      nx = fetch(k + 1);
-      if (k >= S) mbar_wait(&empty[s], static_cast<uint32_t>(((k / S) - 1) & 1));
-      const bool valid = cur.kv >= 0;
-      char* hp = nullptr;
-      char* dp = nullptr;
-      if (valid) row_finish(p, cur, hp, dp);
-      const uint64_t hprev = __shfl_up_sync(kFull, reinterpret_cast<uint64_t>(hp), 1);
-      const int vprev = __shfl_up_sync(kFull, static_cast<int>(valid), 1);
-      const bool head = valid && !(lane > 0 && vprev && hprev + tok == reinterpret_cast<uint64_t>(hp));
-      const unsigned heads = __ballot_sync(kFull, head);
-      const int nvalid = __popc(__ballot_sync(kFull, valid));
-      const unsigned later = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
-      const int run = (later ? __ffs(later) - 1 : nvalid) - lane;
-      tab_addr[s * 32 + lane] = reinterpret_cast<uint64_t>(dp);
-      // lane 0 also announces the stage's bytes; the phase cannot complete before its arrive
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nvalid * tok));
-      else mbar_arrive(&full[s]);
-      __syncwarp();
-      if (head) bulk_g2s(buf + static_cast<size_t>(s) * SB + lane * tok, hp, static_cast<uint32_t>(run * tok),
-                         &full[s]);
-    }
-  } else {
-    // ---------------- consumers ----------------
-    const int ct = threadIdx.x - 32;
-    constexpr int kThreads = 32 * kWsConsumers;
-    const int nvec = T * p.vpt;
-    for (int64_t k = 0; k < my; ++k) {
-      const int s = static_cast<int>(k % S);
-      mbar_wait(&full[s], static_cast<uint32_t>((k / S) & 1));
-      const unsigned char* st = buf + static_cast<size_t>(s) * SB;
-      const uint64_t* tab = tab_addr + s * 32;
-#pragma unroll 4
-      for (int vi = ct; vi < nvec; vi += kThreads) {
-        const int row = vec_row(p, vi);
-        const int w = vi - row * p.vpt;
-        char* d = reinterpret_cast<char*>(tab[row]);
-        if (d) {
-          const int4 val = ld_shared_v4(st + row * tok + w * 16);
-          if (CONTIG) {
-            st_vec(d + w * 16, val);
-          } else {
-            const int h = w / p.vph;
-            st_vec(d + h * p.head_stride + (w - h * p.vph) * 16, val);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -584,12 +402,11 @@ __global__ void __launch_bounds__(1024) ldg_narrow_kernel(const __grid_constant_
 template <int DIR>
 cudaError_t ldg_narrow_launch(const XferParams& p, int ctas, int threads, cudaStream_t s) {
   switch (p.gran) {
-    case 8: ldg_narrow_kernel<8, DIR><<<ctas, threads, 0, s>>>(p); break;
-    case 4: ldg_narrow_kernel<4, DIR><<<ctas, threads, 0, s>>>(p); break;
-    case 2: ldg_narrow_kernel<2, DIR><<<ctas, threads, 0, s>>>(p); break;
-    default: ldg_narrow_kernel<1, DIR><<<ctas, threads, 0, s>>>(p); break;
+    case 8: return launch_k(ldg_narrow_kernel<8, DIR>, ctas, threads, 0, s, p);
+    case 4: return launch_k(ldg_narrow_kernel<4, DIR>, ctas, threads, 0, s, p);
+    case 2: return launch_k(ldg_narrow_kernel<2, DIR>, ctas, threads, 0, s, p);
+    default: return launch_k(ldg_narrow_kernel<1, DIR>, ctas, threads, 0, s, p);
   }
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -627,27 +444,24 @@ __global__ void validate_kernel(const __grid_constant__ ValidateParams v) {
 
 template <int U, int DIR>
 cudaError_t ldg_launch(const XferParams& p, bool contig, bool hcontig, int ctas, int threads, cudaStream_t s) {
-  if (contig && hcontig) ldg_kernel<U, true, true, DIR><<<ctas, threads, 0, s>>>(p);
-  else if (contig) ldg_kernel<U, true, false, DIR><<<ctas, threads, 0, s>>>(p);
-  else if (hcontig) ldg_kernel<U, false, true, DIR><<<ctas, threads, 0, s>>>(p);
-  else ldg_kernel<U, false, false, DIR><<<ctas, threads, 0, s>>>(p);
-  return cudaGetLastError();
+  if (contig && hcontig) return launch_k(ldg_kernel<U, true, true, DIR>, ctas, threads, 0, s, p);
+  else if (contig) return launch_k(ldg_kernel<U, true, false, DIR>, ctas, threads, 0, s, p);
+  else if (hcontig) return launch_k(ldg_kernel<U, false, true, DIR>, ctas, threads, 0, s, p);
+  else return launch_k(ldg_kernel<U, false, false, DIR>, ctas, threads, 0, s, p);
 }
 
 template <int U, int DIR>
 cudaError_t ldg_fused_launch(const FusedParams& p, bool contig, bool hcontig, int ctas, int threads, cudaStream_t s) {
-  if (contig && hcontig) ldg_fused_kernel<U, true, true, DIR><<<ctas, threads, 0, s>>>(p);
-  else if (contig) ldg_fused_kernel<U, true, false, DIR><<<ctas, threads, 0, s>>>(p);
-  else if (hcontig) ldg_fused_kernel<U, false, true, DIR><<<ctas, threads, 0, s>>>(p);
-  else ldg_fused_kernel<U, false, false, DIR><<<ctas, threads, 0, s>>>(p);
-  return cudaGetLastError();
+  if (contig && hcontig) return launch_k(ldg_fused_kernel<U, true, true, DIR>, ctas, threads, 0, s, p);
+  else if (contig) return launch_k(ldg_fused_kernel<U, true, false, DIR>, ctas, threads, 0, s, p);
+  else if (hcontig) return launch_k(ldg_fused_kernel<U, false, true, DIR>, ctas, threads, 0, s, p);
+  else return launch_k(ldg_fused_kernel<U, false, false, DIR>, ctas, threads, 0, s, p);
 }
 
 template <int DIR, bool CONTIG>
 cudaError_t tma_launch(const XferParams& p, int ctas, cudaStream_t s) {
   const int smem = tma_buf_offset(p.tma_stages) + p.tma_stages * p.tma_stage_bytes;
-  tma_kernel<DIR, CONTIG><<<ctas, 32, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(tma_kernel<DIR, CONTIG>, ctas, 32, smem, s, p);
 }
 
 }  // namespace
@@ -675,14 +489,8 @@ cudaError_t launch_ldg_fused(const FusedParams& p, int dir, int ctas, int thread
                   : ldg_fused_launch<8, 1>(p, contig, hcontig, ctas, threads, s);
 }
 
-cudaError_t launch_tma(const XferParams& p, int dir, int ctas, bool warp_specialized, cudaStream_t s) {
+cudaError_t launch_tma(const XferParams& p, int dir, int ctas, cudaStream_t s) {
   const bool contig = dev_contig(p);
-  if (dir == 0 && warp_specialized) {
-    const int smem = tma_buf_offset(p.tma_stages) + p.tma_stages * p.tma_stage_bytes;
-    if (contig) tma_ws_load_kernel<true><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
-    else tma_ws_load_kernel<false><<<ctas, 32 * (1 + kWsConsumers), smem, s>>>(p);
-    return cudaGetLastError();
-  }
   if (dir == 0) return contig ? tma_launch<0, true>(p, ctas, s) : tma_launch<0, false>(p, ctas, s);
   return contig ? tma_launch<1, true>(p, ctas, s) : tma_launch<1, false>(p, ctas, s);
 }
@@ -692,8 +500,7 @@ cudaError_t launch_validate(const ValidateParams& v, cudaStream_t s) {
   int64_t blocks = (v.ntok + threads - 1) / threads;
   if (blocks < 1) blocks = 1;
   if (blocks > 1184) blocks = 1184;
-  validate_kernel<<<static_cast<int>(blocks), threads, 0, s>>>(v);
-  return cudaGetLastError();
+  return launch_k(validate_kernel, static_cast<int>(blocks), threads, 0, s, v);
 }
 
 int tma_smem_limit() {
@@ -707,8 +514,6 @@ int tma_header_bytes(int stages) { return tma_buf_offset(stages); }
 
 cudaError_t tma_prepare(int smem) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(tma_ws_load_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(tma_ws_load_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(tma_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;

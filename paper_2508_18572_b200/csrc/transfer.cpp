@@ -235,6 +235,33 @@ static int run_validate(strata_pool* p, const strata_xfer* x, const Plan& plan, 
   return STRATA_OK;
 }
 
+// STRATA_VALIDATE for STRATA_ENGINE_DMA: the copy engines follow the host mirror of the chunk list
+// while the scatter kernel (and every other engine) follows the device list, so the two must agree
+// over every entry the call reads.
+static int check_host_mirror(strata_pool* p, const strata_xfer* x, const Plan& plan, cudaStream_t s) {
+  const int64_t C = p->d.chunk_tokens;
+  int64_t lo = INT64_MAX, hi = 0;
+  for (int32_t r : plan.reqs) {
+    const int64_t oc = x->chunk_offset ? x->chunk_offset[r] : 0;
+    lo = std::min<int64_t>(lo, x->chunk_start[r]);
+    hi = std::max<int64_t>(hi, x->chunk_start[r] + (oc + x->num_tokens[r] + C - 1) / C);
+  }
+  if (hi <= lo) return STRATA_OK;
+  std::vector<int32_t> dev(size_t(hi - lo));
+  cudaError_t e = cudaMemcpyAsync(dev.data(), x->host_chunks + lo, dev.size() * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(host_chunks check)");
+  for (int32_t r : plan.reqs) {
+    const int64_t oc = x->chunk_offset ? x->chunk_offset[r] : 0;
+    const int64_t a = x->chunk_start[r], b = a + (oc + x->num_tokens[r] + C - 1) / C;
+    for (int64_t i = a; i < b; ++i)
+      if (x->host_chunks_host[i] != dev[size_t(i - lo)])
+        return fail(STRATA_ERR_INVALID_ARG, "host_chunks_host[%lld] = %d but host_chunks[%lld] = %d on the device",
+                    (long long)i, x->host_chunks_host[i], (long long)i, dev[size_t(i - lo)]);
+  }
+  return STRATA_OK;
+}
+
 static bool env_validate() {
   const char* v = getenv("STRATA_VALIDATE");
   return v && *v && strcmp(v, "0") != 0;
@@ -246,6 +273,94 @@ static void count_op(strata_pool* p, const Plan& plan, const strata_xfer* x, int
   p->counters.last_engine = engine;
 }
 
+// Env knob (A/B runs): integer value of `name`, or `def`.
+static int env_int(const char* name, int def) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : def;
+}
+
+// The ring engine needs whole host token rows (token-major tiers, or one head per GPU) in 16-byte
+// units; a head-major tier with several heads per GPU has no whole rows.
+static bool ring_supported(const strata_pool* p) { return p->gran == 16 && p->host_row_contig(); }
+
+// Ring geometry for this pool and direction (rows per piece, stages, scatter warps); false when a
+// 2-stage ring of one-row pieces does not fit in shared memory.
+static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const XferParams& xp, RingParams& rp) {
+  const int tok = static_cast<int>(p->tok_bytes);
+  int W = x->threads ? x->threads / 32 - 1
+                     : dir == 0 ? env_int("STRATA_RING_WARPS", kDefaultRingWarps)
+                                : env_int("STRATA_RING_GATHER_WARPS", kDefaultRingGatherWarps);
+  W = std::max(1, std::min(kRingMaxWarps, W));
+  const int target = std::max(1, env_int("STRATA_RING_STAGE_KB", kDefaultRingStageKB)) << 10;
+  int R = std::min<int>(p->d.chunk_tokens, std::max(1, target / tok));
+  R = std::min(R, std::min(kRingMaxRows, 32 * W));
+  const int sb = (R * tok + 127) / 128 * 128;
+  int budget = p->tma_smem;
+  const int cap_kb = env_int("STRATA_RING_SMEM_KB", 0);
+  if (cap_kb > 0) budget = std::min(budget, cap_kb << 10);
+  int S = std::min(kRingMaxStages, env_int("STRATA_RING_STAGES", kRingMaxStages));
+  while (S >= 2 && ring_header_bytes(S, R) + S * sb > budget) --S;
+  if (S < 2) return false;
+  std::memset(&rp, 0, offsetof(RingParams, pair_end));
+  rp.x = xp;
+  rp.rows = R;
+  rp.stages = S;
+  rp.stage_bytes = sb;
+  rp.pps = (p->d.chunk_tokens + R - 1) / R;
+  rp.warps = W;
+  rp.host_run = p->host_tok_stride == p->tok_bytes;
+  rp.piece_magic = xp.vpt_shift < 0 ? div_magic(xp.vpt, R * xp.vpt) : 0;
+  for (int l = 0; l < p->d.num_layers; ++l) {
+    rp.kb[l] = static_cast<char*>(p->k[l]);
+    rp.vb[l] = static_cast<char*>(p->v[l]);
+  }
+  return true;
+}
+
+// Request table + piece count of one launch; false if the pieces overflow int32.
+static bool ring_batch(const strata_pool* p, const strata_xfer* x, const Plan& plan, const Batch& b, RingParams& rp) {
+  fill_table(x, plan, b, rp.x.rt);
+  rp.x.ntok = b.ntok;
+  const int64_t C = p->d.chunk_tokens;
+  int64_t acc = 0;
+  for (int32_t k = 0; k < b.count; ++k) {
+    const int32_t r = plan.reqs[b.first + k];
+    const int64_t oc = x->chunk_offset ? x->chunk_offset[r] : 0;
+    acc += (oc + x->num_tokens[r] + C - 1) / C;
+    rp.pair_end[k] = static_cast<int32_t>(std::min<int64_t>(acc, INT32_MAX));
+  }
+  const int64_t pieces = acc * p->nkv * rp.pps;
+  if (pieces > INT32_MAX) return false;
+  rp.npieces = static_cast<int32_t>(pieces);
+  return true;
+}
+
+// The op slot's previous fused operation (possibly on another stream) still owns the slot's arrival
+// counters and flags until it completes: order the new fused launch after it (its last-layer event,
+// recorded on its own stream after its kernel).  Almost always already complete, so cheap.
+static cudaError_t order_after_slot(strata_pool* p, const strata_pool::Op& prev, int slot, cudaStream_t s) {
+  if (!prev.fused || !prev.ticket) return cudaSuccess;
+  return cudaStreamWaitEvent(s, p->events[size_t(slot) * (p->d.num_layers + 1) + prev.l1], 0);
+}
+
+// After a fused launch: layer l < l1-1 completes when its device flag reaches the epoch; the side
+// stream of the slot turns each flag into the layer's event.  The last layer completes with the
+// kernel: its event goes on the caller's stream, sparing the op's completion the flag-poll latency.
+static cudaError_t fused_events(strata_pool* p, int slot, const strata_xfer* x, uint32_t* flags, uint32_t epoch,
+                                cudaStream_t s) {
+  const int L = p->d.num_layers;
+  cudaError_t e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + x->layer_end], s);
+  if (e != cudaSuccess) return e;
+  cudaStream_t side = p->side[slot];
+  for (int32_t l = x->layer_begin; l + 1 < x->layer_end; ++l) {
+    if (g_wait_value32(reinterpret_cast<CUstream>(side), reinterpret_cast<CUdeviceptr>(flags + l), epoch,
+                       CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return cudaErrorUnknown;
+    if ((e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], side))) return e;
+  }
+  return cudaSuccess;
+}
+
 int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir) {
   if (!p) return fail(STRATA_ERR_INVALID_ARG, "pool is NULL");
   Plan plan;
@@ -253,9 +368,8 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   if (rc) return rc;
   DeviceGuard dg(p->d.device);
   if (dg.err) return cuda_fail(dg.err, "cudaSetDevice");
-  cudaError_t e = cudaGetLastError();  // surface an earlier asynchronous fault
-  if (e != cudaSuccess) return cuda_fail(e, "earlier CUDA error");
-  if (plan.total_tokens > 0 && ((p->d.flags & STRATA_VALIDATE) || env_validate())) {
+  const bool validate = plan.total_tokens > 0 && ((p->d.flags & STRATA_VALIDATE) || env_validate());
+  if (validate) {
     rc = run_validate(p, x, plan, dir, s);
     if (rc) return rc;
   }
@@ -292,31 +406,26 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.wpr_magic = (xp.wpr & (xp.wpr - 1)) ? div_magic(xp.wpr, 32 * xp.wpr + 32 * 4) : 0;
   xp.wph_magic = (xp.wph & (xp.wph - 1)) ? div_magic(xp.wph, xp.wpr) : 0;
 
+  // Engine.  The default is a hand-written zero-copy kernel reading / writing the host tier through
+  // its UVA mapping: the ring engine where the tier has whole host rows in 16-byte
+  // units, else the LDG engine (narrow rows R29, head-major tiers with several heads per GPU).  The
+  // copy-engine path (STRATA_ENGINE_DMA) runs only when a caller asks for it.
   int engine = x->engine;
-  if (engine == STRATA_ENGINE_DEFAULT) {
-    // Measured on B200: the copy-engine gather + SM scatter moves 98 % of the link
-    // for layer-sized transfers; below a few MiB per layer its per-piece submission latency is not
-    // amortised and the zero-copy LDG kernel wins.  Without a host mirror of the chunk list only
-    // the kernel engines can run.
-    // (Offloads group layers into >= 128 KiB runs inside the DMA engine, see transfer_dma.)
-    // Loads copy one chunk-layer per run (per head for head-major tiers); below ~24 KiB a run the
-    // copy engines fall behind the SM path (72-byte rows at C = 64: 9 KiB runs, DMA 24 vs LDG 33.5
-    // GB/s; tools/narrow_probe.py).  Offloads group layers into >= 128 KiB runs anyway.
-    const int64_t layer_bytes = p->nkv * plan.total_tokens * p->tok_bytes;
-    const int64_t run = int64_t(p->nkv) * p->d.chunk_tokens * (p->head_major ? p->head_bytes : p->tok_bytes);
-    const bool dma = x->host_chunks_host && layer_bytes >= kDmaMinLayerBytes && dma_runs_ok(p) &&
-                     (dir == 1 || run >= kDmaMinLoadRun);
-    engine = dma ? STRATA_ENGINE_DMA : STRATA_ENGINE_LDG;
-  }
+  if (engine == STRATA_ENGINE_DEFAULT) engine = ring_supported(p) ? STRATA_ENGINE_TMA : STRATA_ENGINE_LDG;
   // the copy engines need long host runs: a token-major tier read in a head slice (Ht > H) has
   // only H*D*e bytes per token contiguous, so its DMA requests run on the LDG engine instead
   if (engine == STRATA_ENGINE_DMA && !dma_runs_ok(p)) engine = STRATA_ENGINE_LDG;
   if (engine == STRATA_ENGINE_DMA) {
     if (!x->host_chunks_host && plan.total_tokens > 0)
       return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
+    if (validate && (rc = check_host_mirror(p, x, plan, s))) return rc;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &cap);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
     const uint64_t t = p->next_ticket++;
     const int slot = static_cast<int>(t % kEventRing);
     p->ops[slot] = {t, x->layer_begin, x->layer_end};
+    p->ops[slot].captured = cap != cudaStreamCaptureStatusNone;
     e = cudaEventRecord(p->events[size_t(slot) * (p->d.num_layers + 1)], s);
     if (e != cudaSuccess) {
       p->ops[slot].ticket = 0;   // a failed operation has no valid events
@@ -331,19 +440,16 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     if (ticket) *ticket = t;
     return STRATA_OK;
   }
-  // the TMA rings stage whole host rows in 16-byte units: a head-major tier with > 1 head per GPU
+  RingParams rp;
+  if (engine == STRATA_ENGINE_TMA && !(ring_supported(p) && plan_ring(p, x, dir, xp, rp))) engine = STRATA_ENGINE_LDG;
+  // the bulk rings stage whole host rows in 16-byte units: a head-major tier with > 1 head per GPU
   // has no whole rows, a pool whose rows / strides are not 16-byte multiples (R29) no 16-byte units
-  if ((engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK) && (!p->host_row_contig() || p->gran < 16))
-    engine = STRATA_ENGINE_LDG;
-  const bool tma = engine == STRATA_ENGINE_TMA || engine == STRATA_ENGINE_TMA_BULK;
-  // TMA engine geometry: rows per stage (<= 32 lanes), stage bytes, depth
-  if (tma) {
-    // the warp-specialised ring is producer-bound per stage: larger stages (64 KiB) amortise it
-    const int target = engine == STRATA_ENGINE_TMA ? 2 * kTmaStageTarget : kTmaStageTarget;
-    int rows = std::max(1, std::min(32, target / xp.tok_bytes));
+  if (engine == STRATA_ENGINE_TMA_BULK && (!p->host_row_contig() || p->gran < 16)) engine = STRATA_ENGINE_LDG;
+  if (engine == STRATA_ENGINE_TMA_BULK) {
+    const int rows = std::max(1, std::min(32, kTmaStageTarget / xp.tok_bytes));
     const int sb = rows * xp.tok_bytes;
     const int budget = p->tma_smem - strata::tma_header_bytes(strata::kTmaMaxStages);
-    int stages = std::min(strata::kTmaMaxStages, budget / sb);
+    const int stages = std::min(strata::kTmaMaxStages, budget / sb);
     if (stages < 2) {
       engine = STRATA_ENGINE_LDG;  // token rows too large for a 2-stage shared-memory ring
     } else {
@@ -354,22 +460,28 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   }
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;   // U=8 is compiled for <= 512 threads
-  // lane t fetches row t; the warp then streams the 32 rows (amortised index math).  The narrow
-  // kernel (R29) takes one row per warp, so its grid is sized per row.
+  // lane t fetches row t; the warp then streams the 32 rows (amortised index math)
   xp.rows_per_group = 32;
-  int ctas = x->num_ctas ? x->num_ctas
-             : engine != STRATA_ENGINE_LDG ? kDefaultCtasTma
-             : p->gran < 16                ? kDefaultCtasNarrow
-             : dir == 0                    ? kDefaultCtasLdg
-                                           : kDefaultCtasLdgOffload;
-  // small token rows shrink a TMA stage (<= 32 rows); keep ~64 KiB per stage-CTA in flight by
-  // spreading over more CTAs (70B TP=8: 256 B rows -> 8 KiB stages -> 16 CTAs)
-  if (!x->num_ctas && engine != STRATA_ENGINE_LDG && xp.tma_stage_bytes > 0)
-    ctas = std::min(16, ctas * std::max(1, (2 * kTmaStageTarget) / xp.tma_stage_bytes));
+  int ctas = x->num_ctas;
+  if (!ctas) {
+    if (engine == STRATA_ENGINE_TMA) ctas = dir == 0 ? kDefaultCtasRingLoad : kDefaultCtasRingOffload;
+    else if (engine == STRATA_ENGINE_TMA_BULK) ctas = kDefaultCtasTma;
+    else if (p->gran < 16) ctas = kDefaultCtasNarrow;
+    else ctas = dir == 0 ? kDefaultCtasLdg : kDefaultCtasLdgOffload;
+    // small token rows shrink a bulk stage (<= 32 rows); keep ~64 KiB per stage-CTA in flight by
+    // spreading over more CTAs (70B TP=8: 256 B rows -> 8 KiB stages -> 16 CTAs)
+    if (engine == STRATA_ENGINE_TMA_BULK && xp.tma_stage_bytes > 0)
+      ctas = std::min(16, ctas * std::max(1, (2 * kTmaStageTarget) / xp.tma_stage_bytes));
+  }
 
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &cap);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamIsCapturing");
   const uint64_t t = p->next_ticket++;
   const int slot = static_cast<int>(t % kEventRing);
+  const strata_pool::Op prev = p->ops[slot];
   p->ops[slot] = {t, x->layer_begin, x->layer_end};
+  p->ops[slot].captured = cap != cudaStreamCaptureStatusNone;
   const int L = p->d.num_layers;
   // a failed operation keeps no ticket: its ring slot must not hand out stale events
   auto op_fail = [&](cudaError_t err, const char* what) {
@@ -379,50 +491,72 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   e = cudaEventRecord(p->events[size_t(slot) * (L + 1)], s);  // operation start
   if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
   // One launch for all layers when the call is one request table and not being captured (stream
-  // memory operations are not captured here); layer events come from the device flags.  Measured
-  // (profiles/r01/fused_ab_*.jsonl): +2 % at the default 2 CTAs (51.2 GB/s, 99.4 % of the SM
-  // zero-copy ceiling), +0.5 % at 4, but -3..-7 % with a single CTA, so 1-CTA grids keep the
-  // per-layer launches.
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  // memory operations are not captured here); layer events come from the device flags.
+  const bool can_fuse = plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 && L <= kMaxFusedLayers &&
+                        fused_mode() && cap == cudaStreamCaptureStatusNone && ensure_fused(p);
+  uint32_t* counters = p->fused_sync + size_t(slot) * 2 * L;
+  if (engine == STRATA_ENGINE_TMA) {
+    if (can_fuse) {
+      if (!ring_batch(p, x, plan, plan.batches[0], rp)) return op_fail(cudaErrorInvalidValue, "ring piece count");
+      const int c = std::max(1, std::min(ctas, rp.npieces));
+      rp.l0 = x->layer_begin;
+      rp.l1 = x->layer_end;
+      rp.epoch = static_cast<uint32_t>(t);
+      rp.arrivals = dir == 0 ? c * rp.warps : c;
+      rp.counters = counters;
+      rp.flags = counters + L;
+      if ((e = order_after_slot(p, prev, slot, s))) return op_fail(e, "cudaStreamWaitEvent(slot)");
+      if ((e = strata::launch_ring(rp, dir, c, s))) return op_fail(e, "ring kernel launch");
+      p->ops[slot].fused = true;
+      ++p->counters.kernel_launches;
+      if ((e = fused_events(p, slot, x, rp.flags, rp.epoch, s))) return op_fail(e, "layer events");
+      count_op(p, plan, x, engine);
+      if (ticket) *ticket = t;
+      return STRATA_OK;
+    }
+    // per layer (graph capture, several request tables, one layer): one launch per layer and table
+    for (int32_t l = x->layer_begin; l < x->layer_end; ++l) {
+      for (const Batch& b : plan.batches) {
+        if (!ring_batch(p, x, plan, b, rp)) return op_fail(cudaErrorInvalidValue, "ring piece count");
+        const int c = std::max(1, std::min(ctas, rp.npieces));
+        rp.l0 = l;
+        rp.l1 = l + 1;
+        if ((e = strata::launch_ring(rp, dir, c, s))) return op_fail(e, "ring kernel launch");
+        ++p->counters.kernel_launches;
+      }
+      if ((e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], s))) return op_fail(e, "cudaEventRecord");
+    }
+    count_op(p, plan, x, engine);
+    if (ticket) *ticket = t;
+    return STRATA_OK;
+  }
+  // LDG: one launch for all layers from 2 CTAs (measured, profiles/r01/fused_ab_*.jsonl: +2 % at
+  // 2 CTAs, +0.5 % at 4, but -3..-7 % with a single CTA, so 1-CTA grids keep per-layer launches)
   const int64_t fgroups = plan.batches.empty() ? 0
                               : (int64_t(p->nkv) * plan.batches[0].ntok + xp.rows_per_group - 1) / xp.rows_per_group;
   const int fctas = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctas, (fgroups * 32 + threads - 1) / threads)));
-  if (engine == STRATA_ENGINE_LDG && p->gran == 16 && plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 &&
-      (fctas >= 2 || fused_mode() == 2) && L <= kMaxFusedLayers && fused_mode() && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
-      cap == cudaStreamCaptureStatusNone && ensure_fused(p)) {
+  if (engine == STRATA_ENGINE_LDG && p->gran == 16 && can_fuse && (fctas >= 2 || fused_mode() == 2)) {
     const Batch& b = plan.batches[0];
     FusedParams fp;
     std::memset(&fp, 0, sizeof fp);
     fp.x = xp;
     fp.x.ntok = b.ntok;
     fill_table(x, plan, b, fp.x.rt);
-    const int c = fctas;
     fp.l0 = x->layer_begin;
     fp.l1 = x->layer_end;
     fp.epoch = static_cast<uint32_t>(t);
-    fp.total_warps = c * threads / 32;
-    fp.counters = p->fused_sync + size_t(slot) * 2 * L;
-    fp.flags = fp.counters + L;
+    fp.total_warps = fctas * threads / 32;
+    fp.counters = counters;
+    fp.flags = counters + L;
     for (int l = 0; l < L; ++l) {
       fp.kb[l] = static_cast<char*>(p->k[l]);
       fp.vb[l] = static_cast<char*>(p->v[l]);
     }
-    e = strata::launch_ldg_fused(fp, dir, c, threads, s);
-    if (e != cudaSuccess) return op_fail(e, "fused transfer kernel launch");
+    if ((e = order_after_slot(p, prev, slot, s))) return op_fail(e, "cudaStreamWaitEvent(slot)");
+    if ((e = strata::launch_ldg_fused(fp, dir, fctas, threads, s))) return op_fail(e, "fused transfer kernel launch");
     p->ops[slot].fused = true;
     ++p->counters.kernel_launches;
-    cudaStream_t side = p->side[slot];
-    // the last layer completes with the kernel: its event goes on the caller's stream, sparing the
-    // op's completion the side stream's flag-poll latency
-    e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + x->layer_end], s);
-    if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
-    for (int32_t l = x->layer_begin; l + 1 < x->layer_end; ++l) {
-      if (g_wait_value32(reinterpret_cast<CUstream>(side), reinterpret_cast<CUdeviceptr>(fp.flags + l), fp.epoch,
-                         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-        return op_fail(cudaErrorUnknown, "cuStreamWaitValue32");
-      e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], side);
-      if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
-    }
+    if ((e = fused_events(p, slot, x, fp.flags, fp.epoch, s))) return op_fail(e, "layer events");
     count_op(p, plan, x, engine);
     if (ticket) *ticket = t;
     return STRATA_OK;
@@ -436,10 +570,10 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
       fill_table(x, plan, b, xp.rt);
       const int64_t rows = int64_t(p->nkv) * b.ntok;
       int c = ctas;
-      if (engine != STRATA_ENGINE_LDG) {
+      if (engine == STRATA_ENGINE_TMA_BULK) {
         const int64_t pieces = (rows + xp.tma_rows - 1) / xp.tma_rows;
         if (pieces < c) c = static_cast<int>(pieces);
-        e = strata::launch_tma(xp, dir, c, engine == STRATA_ENGINE_TMA, s);
+        e = strata::launch_tma(xp, dir, c, s);
       } else {
         const int64_t groups = (rows + xp.rows_per_group - 1) / xp.rows_per_group;
         const int64_t need = (groups * 32 + threads - 1) / threads;

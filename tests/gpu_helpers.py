@@ -11,6 +11,17 @@ import oracle
 from tests.helpers import CANARY
 
 
+def default_engine(g, strides=None) -> int:
+    """The engine strata_load/offload pick with STRATA_ENGINE_DEFAULT (transfer.cpp): the ring engine
+    (STRATA_ENGINE_TMA) when the tier has whole 16-byte host rows, else LDG (narrow rows R29, or a
+    head-major tier with several heads per GPU)."""
+    import paper_2508_18572_b200 as st
+    vals = [g.H * g.D * g.e, g.D * g.e] + list(strides or ())
+    if any(v % 16 for v in vals) or (getattr(g, "head_major", False) and g.H > 1):
+        return st.STRATA_ENGINE_LDG
+    return st.STRATA_ENGINE_TMA
+
+
 def nhd(g):
     tok = g.H * g.D * g.e
     return (g.P * tok, tok, g.D * g.e)

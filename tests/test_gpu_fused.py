@@ -114,3 +114,45 @@ def test_concurrent_ops_cross_waits():
         assert c.pool.layer_elapsed_ms(tb, g.L - 1) > 0
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("engine", [st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_LDG])
+def test_event_ring_slot_reuse_never_fires_early(engine):
+    """Nine fused loads on two streams, the first held back behind a spin kernel: op 1 and op 9 share
+    an event-ring slot (kEventRing = 8) and so its arrival counters and layer flags.  Op 9 must be
+    ordered after op 1 (transfer.cpp order_after_slot), so no layer event of op 1 fires before its
+    bytes land: a consumer that waits on op 1's layer events checksums exactly the final (oracle)
+    bytes of op 1's pages, and nothing hangs (the executor waits per layer)."""
+    g = Geometry(4, 8, 128, 2, 1, 64, 17000, 300)
+    ns = [8192] + [1024] * 8      # >= 1024 tokens: the LDG engine fuses (>= 2 CTAs) as well
+    q = kvgen.make_requests(kvgen.rng_for(33), ns, g.P, g.C, g.num_pages, g.num_chunks)   # disjoint pages
+    c = GpuCase(g, q)
+    try:
+        def one(r):
+            cs, ps = int(q.chunk_start[r]), int(q.page_start[r])
+            nc, npg = kvgen.chunks_needed(0, ns[r], g.C), kvgen.pages_needed(0, ns[r], g.P)
+            return st.Requests([ns[r]], q.host_chunks[cs: cs + nc], [0], q.dev_pages[ps: ps + npg], [0])
+        reqs = [one(r) for r in range(len(ns))]
+        s1, s2, cons = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        with torch.cuda.stream(s1):
+            torch.cuda._sleep(50_000_000)     # ~25 ms: op 1 starts long after ops 2..9 could
+        t1 = c.pool.load(reqs[0], stream=s1, engine=engine)
+        tickets = [c.pool.load(r, stream=s2, engine=engine) for r in reqs[1:]]
+        assert tickets[-1] == t1 + 8
+        pages1 = torch.from_numpy(q.dev_pages[: ns[0]].astype(np.int64)).cuda()
+        sums = []
+        with torch.cuda.stream(cons):
+            for l in range(g.L):
+                c.pool.wait_layer(t1, l, cons)
+                rows_k = c.k[l].view(g.num_pages, -1)[pages1].view(torch.int64).sum()
+                rows_v = c.v[l].view(g.num_pages, -1)[pages1].view(torch.int64).sum()
+                sums.append((rows_k, rows_v))
+        torch.cuda.synchronize()
+        c.check_load(0, g.L)
+        p1 = q.dev_pages[: ns[0]]
+        for l in range(g.L):
+            ek = c.k[l].cpu().numpy().reshape(g.num_pages, -1)[p1].view(np.int64).sum()
+            ev = c.v[l].cpu().numpy().reshape(g.num_pages, -1)[p1].view(np.int64).sum()
+            assert int(sums[l][0]) == int(ek) and int(sums[l][1]) == int(ev), f"layer {l}: event fired early"
+    finally:
+        c.close()

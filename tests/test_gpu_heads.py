@@ -8,7 +8,7 @@ import pytest
 
 import kvgen
 from kvgen import Geometry
-from tests.gpu_helpers import GpuCase
+from tests.gpu_helpers import GpuCase, default_engine
 
 pytestmark = pytest.mark.gpu
 
@@ -55,16 +55,15 @@ def test_head_slice_small(engine, head_major, H, Ht, h0):
 @pytest.mark.parametrize("head_major", [False, True])
 @pytest.mark.parametrize("H,Ht,h0", [(1, 8, 5), (8, 8, 0)])
 def test_head_slice_layer_sized_default_engine(head_major, H, Ht, h0):
-    """>= 4 MiB per layer: the default engine picks the copy-engine path where the layout has long
-    runs (head-major, or a tier holding only this GPU's heads) and LDG otherwise."""
+    """>= 4 MiB per layer: the default engine is zero-copy: the ring engine where the tier has whole
+    host rows (token-major, or one head per GPU), LDG for a head-major tier with several heads."""
     n = 9000 if H == 1 else 1200
     g = Geometry(L=2, H=H, D=128, e=2, P=1, C=64, num_pages=n + 2000, num_chunks=n // 64 + 20, Ht=Ht, h0=h0,
                  head_major=head_major)
     q = kvgen.make_requests(kvgen.rng_for(80), [n - 100, 90], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
     assert 2 * sum(q.num_tokens) * g.token_bytes >= 4 << 20
     used = _run(g, q, st.STRATA_ENGINE_DEFAULT, seed=3)
-    expect_dma = head_major or Ht == H
-    assert used == (st.STRATA_ENGINE_DMA if expect_dma else st.STRATA_ENGINE_LDG), used
+    assert used == default_engine(g), used
 
 
 @pytest.mark.parametrize("i", range(40))
@@ -130,7 +129,7 @@ def test_llama70b_tp8_shared_tier_bench_config():
     try:
         c.pool.load(c.reqs)
         torch.cuda.synchronize()
-        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_DMA
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_TMA
         c.check_load(0, g.L, layers=[0, 41, 79])
     finally:
         c.close()

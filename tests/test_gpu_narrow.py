@@ -63,25 +63,24 @@ def test_narrow_layouts(engine, layout):
     _run(g, q, engine, strides=strides, seed=3)
 
 
-@pytest.mark.parametrize("C,expect_load", [(64, st.STRATA_ENGINE_LDG), (256, st.STRATA_ENGINE_DMA)])
-def test_narrow_layer_sized_default_engine(C, expect_load):
-    """>= 4 MiB per layer of 72-byte fp8 rows: loads take the copy engines only when a chunk-layer
-    run reaches 24 KiB (C = 256: 36 KiB; C = 64: 9 KiB -> the narrow LDG kernel); offloads group
-    layers and take the copy engines either way, the narrow kernel gathering the staged rows."""
+@pytest.mark.parametrize("C", [64, 256])
+def test_narrow_layer_sized_default_engine(C):
+    """>= 4 MiB per layer of 72-byte fp8 rows: the default engine is the narrow zero-copy LDG kernel
+    in both directions (the copy engines run only when a caller asks for STRATA_ENGINE_DMA)."""
     g = Geometry(L=2, H=1, D=72, e=1, P=1, C=C, num_pages=40000, num_chunks=38400 // C)
     q = kvgen.make_requests(kvgen.rng_for(121), [32000], g.P, g.C, g.num_pages, g.num_chunks)
     c = GpuCase(g, q, seed=4)
     try:
         c.pool.load(c.reqs)
         torch.cuda.synchronize()
-        assert c.pool.counters()["last_engine"] == expect_load
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_LDG
         c.check_load(0, g.L)
         before = c.pool.host.copy()
         for t in c.k + c.v:
             t.copy_(torch.randint(0, 256, t.shape, dtype=torch.uint8, device="cuda"))
         c.pool.offload(c.reqs)
         torch.cuda.synchronize()
-        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_DMA
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_LDG
         assert np.array_equal(c.pool.host, c.expected_offload(before, 0, g.L))
     finally:
         c.close()
