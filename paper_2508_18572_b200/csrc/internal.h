@@ -102,7 +102,7 @@ struct FusedParams {
 //   request, kv); pair -> request by binary search over pair_end.
 constexpr int kRingMaxStages = 16;
 constexpr int kRingMaxWarps = 16;   // LSU scatter warps of a load CTA
-constexpr int kRingMaxRows = 128;   // rows per piece
+constexpr int kRingMaxRows = 64;    // rows per piece (2 per lane of the piece's warp)
 struct RingParams {
   XferParams x;                 // geometry, index lists, request table (kbase/vbase/layer_off unused)
   int32_t l0, l1;               // layer range
@@ -110,20 +110,20 @@ struct RingParams {
   int32_t arrivals;             // arrivals per layer: load = CTAs * warps, offload = CTAs
   uint32_t* counters;           // [L] arrival counters of the op slot, or NULL: no per-layer flags
   uint32_t* flags;              // [L] completion flags of the op slot
-  int32_t rows;                 // R: rows per piece (<= kRingMaxRows, <= 32 * warps)
+  int32_t rows;                 // R: rows per piece (<= kRingMaxRows)
   int32_t stages;               // S: ring depth (<= kRingMaxStages)
   int32_t stage_bytes;          // bytes per stage (R * tok rounded up to 128)
   int32_t pps;                  // pieces per segment = ceil(C / R)
   int32_t npieces;              // pieces per layer
   int32_t host_run;             // 1: a piece's host rows are one contiguous run (host_tok_stride == tok)
   int32_t warps;                // device-side LSU warps per CTA: load scatter / offload gather (+1 TMA warp)
-  uint32_t piece_magic;         // row of vector v < R*vpt: umulhi(v, magic) (0: vpt_shift or divide)
+  int32_t bulk_store;           // load: the device side as cp.async.bulk stores instead of st.global
   int32_t pair_end[kMaxReqsPerLaunch];   // inclusive prefix sums of chunk positions per request
   char* kb[kMaxFusedLayers];    // per-layer K / V bases
   char* vb[kMaxFusedLayers];
 };
-// Shared-memory bytes in front of the ring's stages (mbarriers + per-stage row-address tables).
-int ring_header_bytes(int stages, int rows);
+// Shared-memory bytes in front of the ring's stages (mbarriers).
+int ring_header_bytes();
 cudaError_t launch_ring(const RingParams& p, int dir, int ctas, cudaStream_t s);
 cudaError_t ring_prepare(int smem);
 

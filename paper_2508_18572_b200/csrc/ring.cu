@@ -12,8 +12,8 @@
 //   load    warp 0       producer: one bulk host -> stage copy per piece (or one per row when the
 //                        host rows of a piece are strided: a head slice of a wider token-major tier)
 //           warps 1..W   scatter: ld.shared.v4 -> st.global.v4 to the rows' pages (16-byte vectors,
-//                        U in flight per lane), row addresses from a per-stage table they fill one
-//                        piece ahead (page-table index loads issued a piece early)
+//                        U in flight per lane); warp w owns pieces w, w+W, ... and loads their
+//                        page-table entries two of its pieces ahead
 //   offload warp 0       store: one bulk stage -> host copy per piece; a stage is released when its
 //                        store has read shared memory (cp.async.bulk.wait_group.read)
 //           warps 1..W   gather: 16-byte cp.async from the rows' pages into the stage, completion
@@ -37,10 +37,8 @@ using namespace dev;
 constexpr int kRingBarBytes = 2 * kRingMaxStages * 8;   // full[16], empty[16]
 constexpr int kU = 4;                                   // 16-byte vectors in flight per scatter lane
 
-// [full[16] | empty[16] | row-address table [S][R] | pad to 128 | S stages]
-__host__ __device__ constexpr int ring_buf_offset(int stages, int rows) {
-  return (kRingBarBytes + stages * rows * 8 + 127) / 128 * 128;
-}
+// [full[16] | empty[16] | pad to 128 | S stages]
+__host__ __device__ constexpr int ring_buf_offset() { return (kRingBarBytes + 127) / 128 * 128; }
 
 struct Piece {
   int32_t r;    // request in the launch table
@@ -103,16 +101,6 @@ __device__ __forceinline__ uint64_t row_addr(const RingParams& p, const RowPre& 
   return rp.pg < 0 ? 0 : rp.base + uint64_t(int64_t(rp.pg) * p.x.page_stride);
 }
 
-__device__ __forceinline__ int piece_row(const RingParams& p, int v) {
-  if (p.x.vpt_shift >= 0) return v >> p.x.vpt_shift;
-  if (p.piece_magic) return static_cast<int>(__umulhi(static_cast<unsigned>(v), p.piece_magic));
-  return v / p.x.vpt;
-}
-
-__device__ __forceinline__ void named_sync(int id, int threads) {
-  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(threads) : "memory");
-}
-
 // Layer l complete for this arriver: the last of p.arrivals resets the counter (for the op slot's
 // next operation, which the host orders after this one) and publishes the epoch.
 template <int DIR>
@@ -126,40 +114,155 @@ __device__ __forceinline__ void arrive_layer(const RingParams& p, int l) {
   }
 }
 
-// Page-index lookahead of the device-side warps: every thread keeps the (page, base) of its row for
-// the next kLook pieces in registers, so a piece's page-table loads were issued kLook pieces earlier
-// (one piece of lookahead left ~0.6-0.9 us of index latency on each piece's critical path:
-// profiles/r02/ring_sweep1.jsonl, 1-CTA rate proportional to the piece size).
-constexpr int kLook = 4;
+// Device-side warps own whole PIECES: the CTA's piece q (its sequence number over the operation) goes
+// to warp q % W, which moves all of its rows (lane j holds the (page, base) of rows j and j + 32;
+// R <= 64).  The host side makes W divide the ring depth S, so stage s is always drained (load) or
+// filled (offload) by warp s % W: a warp then waits on each of its stages' barriers one phase at a
+// time, never two phases ahead (mbarrier parity waits cannot tell phase k from phase k + 2).  Every warp runs its
+// own pieces' latency chains (page-table loads issued kLook of its pieces early, the stage wait, the
+// row loop), so W pieces drain at once.  (All warps on every piece, with a shared row-address table
+// and a named barrier per piece, left the 1-CTA kernel issue-latency bound at ~27-37 GB/s:
+// profiles/r02/ncu_ring_load_1cta_v1.txt, ring_sweep4.jsonl.)
+constexpr int kLook = 2;
+constexpr int kRowsPerLane = kRingMaxRows / 32;
 
 struct RowQueue {
-  RowPre r[kLook];
+  RowPre r[kLook][kRowsPerLane];
   int32_t n[kLook];
 };
 
-__device__ __forceinline__ void rowq_set(const RingParams& p, RowQueue& q, int i, int32_t m, int32_t mine, int t,
+__device__ __forceinline__ void rowq_set(const RingParams& p, RowQueue& q, int i, int32_t m, int32_t mine, int lane,
                                          char* kb, char* vb) {
   const int G = gridDim.x;
   const Piece pc = m < mine ? piece_of(p, blockIdx.x + m * G) : Piece{0, 0, 0, 0, 0};
-  q.r[i] = row_pre(p, pc, t, kb, vb);
+#pragma unroll
+  for (int c = 0; c < kRowsPerLane; ++c) q.r[i][c] = row_pre(p, pc, lane + 32 * c, kb, vb);
   q.n[i] = pc.n;
 }
-__device__ __forceinline__ void rowq_init(const RingParams& p, RowQueue& q, int32_t mine, int t, char* kb, char* vb) {
+// warp wi's pieces of a layer: m = wi, wi + W, ...; queue slot i holds the warp's i-th next piece
+__device__ __forceinline__ void rowq_init(const RingParams& p, RowQueue& q, int32_t m0, int32_t mine, int lane,
+                                          char* kb, char* vb) {
 #pragma unroll
-  for (int i = 0; i < kLook; ++i) rowq_set(p, q, i, i, mine, t, kb, vb);
+  for (int i = 0; i < kLook; ++i) rowq_set(p, q, i, m0 + i * p.warps, mine, lane, kb, vb);
 }
-// pops the head (piece m) and issues the index loads of piece m + kLook
-__device__ __forceinline__ RowPre rowq_pop(const RingParams& p, RowQueue& q, int32_t m, int32_t mine, int t,
-                                           char* kb, char* vb, int& n) {
-  const RowPre head = q.r[0];
+// pops the head (piece m) and issues the index loads of the warp's piece kLook ahead
+__device__ __forceinline__ void rowq_pop(const RingParams& p, RowQueue& q, int32_t m, int32_t mine, int lane,
+                                         char* kb, char* vb, uint64_t (&addr)[kRowsPerLane], int& n) {
+#pragma unroll
+  for (int c = 0; c < kRowsPerLane; ++c) addr[c] = row_addr(p, q.r[0][c]);
   n = q.n[0];
 #pragma unroll
   for (int i = 0; i + 1 < kLook; ++i) {
-    q.r[i] = q.r[i + 1];
+#pragma unroll
+    for (int c = 0; c < kRowsPerLane; ++c) q.r[i][c] = q.r[i + 1][c];
     q.n[i] = q.n[i + 1];
   }
-  rowq_set(p, q, kLook - 1, m + kLook, mine, t, kb, vb);
-  return head;
+  rowq_set(p, q, kLook - 1, m + kLook * p.warps, mine, lane, kb, vb);
+}
+
+// Row j's device address, held by lane j % 32 in slot j / 32.
+__device__ __forceinline__ uint64_t row_base(const uint64_t (&addr)[kRowsPerLane], int j) {
+  uint64_t v = addr[0];
+#pragma unroll
+  for (int c = 1; c < kRowsPerLane; ++c)
+    if ((j >> 5) == c) v = addr[c];
+  return __shfl_sync(kFull, v, j & 31);
+}
+
+// Every (row, 16-byte vector) of one piece by one warp.  Wide rows (vpt >= 32): one row at a time,
+// lane c covers vectors c, c+32, ...; narrow rows: 32 / vpt rows per instruction, lane = (row slot,
+// vector).  kU vectors per lane are batched so their shared / global accesses overlap.
+//   DIR 0 (load):    stage -> registers -> page rows (ld.shared.v4 / st.global.v4)
+//   DIR 1 (offload): page rows -> stage (cp.async, completion counted on the stage's barrier)
+template <bool CONTIG, int DIR>
+__device__ __forceinline__ void piece_rows(const RingParams& p, int lane, int n, const uint64_t (&addr)[kRowsPerLane],
+                                           unsigned char* st) {
+  const XferParams& x = p.x;
+  const int vpt = x.vpt, tok = x.tok_bytes;
+  if (vpt >= 32) {
+    for (int j = 0; j < n; ++j) {
+      const uint64_t base = row_base(addr, j);
+      unsigned char* srow = st + j * tok;
+      for (int c0 = 0; c0 < vpt; c0 += 32 * kU) {
+        if (DIR == 0) {
+          int4 val[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int c = c0 + u * 32 + lane;
+            if (c < vpt) val[u] = ld_shared_v4(srow + c * 16);
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int c = c0 + u * 32 + lane;
+            if (c < vpt) st_vec(reinterpret_cast<void*>(row_vec<CONTIG>(base, c, x, x.head_stride)), val[u]);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int c = c0 + u * 32 + lane;
+            if (c < vpt) cp_async16(srow + c * 16, reinterpret_cast<const void*>(row_vec<CONTIG>(base, c, x, x.head_stride)));
+          }
+        }
+      }
+    }
+  } else {
+    const int rpi = 32 / vpt;             // rows per warp instruction
+    const int lr = lane / vpt, lc = lane - lr * vpt;
+    const bool on = lr < rpi;
+    for (int j0 = 0; j0 < n; j0 += rpi * kU) {
+      int4 val[kU];
+      uint64_t dst[kU];
+      bool ok[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = j0 + u * rpi + lr;
+        const uint64_t base = row_base(addr, j & (kRingMaxRows - 1));
+        ok[u] = on && j < n;
+        dst[u] = row_vec<CONTIG>(base, lc, x, x.head_stride);
+        unsigned char* sv = st + j * tok + lc * 16;
+        if (DIR == 0) {
+          if (ok[u]) val[u] = ld_shared_v4(sv);
+        } else {
+          if (ok[u]) cp_async16(sv, reinterpret_cast<const void*>(dst[u]));
+        }
+      }
+      if (DIR == 0) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (ok[u]) st_vec(reinterpret_cast<void*>(dst[u]), val[u]);
+      }
+    }
+  }
+}
+
+// Load variant (p.bulk_store): the piece's rows leave the stage as cp.async.bulk stores, one per run of
+// rows that are adjacent on the device (a page of P >= 2 tokens) — fewer, larger requests on the SM's
+// path to L2 than 16-byte st.global (which the 1-CTA load saturates: profiles/r02/ncu_ring_load_1cta_v4.txt).
+template <bool CONTIG>
+__device__ __forceinline__ void piece_rows_bulk(const RingParams& p, int lane, int n, const uint64_t (&addr)[kRowsPerLane],
+                                                unsigned char* st) {
+  const XferParams& x = p.x;
+  const int tok = x.tok_bytes;
+#pragma unroll
+  for (int c = 0; c < kRowsPerLane; ++c) {
+    if (32 * c >= n) break;
+    const int j = lane + 32 * c;
+    const uint64_t a = addr[c];
+    if (CONTIG) {
+      const uint64_t prev = __shfl_up_sync(kFull, a, 1);
+      const bool head = j < n && !(lane > 0 && prev && prev + tok == a);
+      const unsigned heads = __ballot_sync(kFull, head);
+      const int lim = min(32, n - 32 * c);
+      const unsigned later = lane == 31 ? 0u : (heads & ~((2u << lane) - 1u));
+      const int run = (later ? __ffs(later) - 1 : lim) - lane;
+      if (head) bulk_s2g(reinterpret_cast<void*>(a), st + j * tok, static_cast<uint32_t>(run * tok));
+    } else if (j < n) {
+      for (int h = 0; h < x.H; ++h)
+        bulk_s2g(reinterpret_cast<char*>(a) + int64_t(h) * x.head_stride, st + j * tok + h * x.head_bytes,
+                 static_cast<uint32_t>(x.head_bytes));
+    }
+  }
+  bulk_commit();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -169,15 +272,14 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(
   const XferParams& x = p.x;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kRingMaxStages;
-  uint64_t* table = reinterpret_cast<uint64_t*>(smem + kRingBarBytes);   // [S][R] device row addresses
-  unsigned char* buf = smem + ring_buf_offset(p.stages, p.rows);
-  const int S = p.stages, R = p.rows, SB = p.stage_bytes, tok = x.tok_bytes;
+  unsigned char* buf = smem + ring_buf_offset();
+  const int S = p.stages, SB = p.stage_bytes, tok = x.tok_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, b = blockIdx.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], p.warps);
+      mbar_init(&empty[s], 1);   // the piece's scatter warp
     }
     mbar_init_fence();
   }
@@ -219,43 +321,34 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(
       }
     }
   } else {
-    // ---------------- scatter warps: stage -> pages ----------------
-    const int ct = threadIdx.x - 32, nct = p.warps * 32;
-    uint32_t q = 0;
+    // ---------------- scatter warps: stage -> pages (warp wi: pieces q == wi mod W) ----------------
+    const int wi = warp - 1, W = p.warps;
     for (int l = p.l0; l < p.l1; ++l) {
       char* kb = p.kb[l];
       char* vb = p.vb[l];
+      const uint32_t q0 = static_cast<uint32_t>(l - p.l0) * static_cast<uint32_t>(mine);
+      const int32_t mfirst = static_cast<int32_t>((static_cast<uint32_t>(wi) + W - q0 % W) % W);   // q = q0 + m == wi (mod W)
       RowQueue rq;
-      rowq_init(p, rq, mine, ct, kb, vb);
-      for (int32_t m = 0; m < mine; ++m, ++q) {
+      rowq_init(p, rq, mfirst, mine, lane, kb, vb);
+      for (int32_t m = mfirst; m < mine; m += W) {
+        const uint32_t q = q0 + m;
         const int s = static_cast<int>(q % S);
         int n;
-        const RowPre cur = rowq_pop(p, rq, m, mine, ct, kb, vb, n);
-        if (ct < R) table[s * R + ct] = row_addr(p, cur);
-        named_sync(1, nct);
+        uint64_t addr[kRowsPerLane];
+        rowq_pop(p, rq, m, mine, lane, kb, vb, addr, n);
         mbar_wait(&full[s], (q / S) & 1);
-        const unsigned char* st = buf + static_cast<size_t>(s) * SB;
-        const uint64_t* tab = table + s * R;
-        const int nvec = n * x.vpt;
-        for (int v0 = ct; v0 < nvec; v0 += nct * kU) {
-          int4 val[kU];
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int v = v0 + u * nct;
-            if (v < nvec) val[u] = ld_shared_v4(st + v * 16);
-          }
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int v = v0 + u * nct;
-            if (v < nvec) {
-              const int row = piece_row(p, v);
-              const int w = v - row * x.vpt;
-              st_vec(reinterpret_cast<void*>(row_vec<CONTIG>(tab[row], w, x, x.head_stride)), val[u]);
-            }
-          }
+        if (p.bulk_store) {
+          piece_rows_bulk<CONTIG>(p, lane, n, addr, buf + static_cast<size_t>(s) * SB);
+          bulk_wait_read<0>();   // the TMA has read this stage
+        } else {
+          piece_rows<CONTIG, 0>(p, lane, n, addr, buf + static_cast<size_t>(s) * SB);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      if (p.bulk_store) {
+        bulk_wait_all();         // the layer's bulk stores are performed
+        fence_proxy_async_global();
       }
       if (p.counters) {
         __syncwarp();
@@ -278,14 +371,13 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
   const XferParams& x = p.x;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kRingMaxStages;
-  uint64_t* table = reinterpret_cast<uint64_t*>(smem + kRingBarBytes);   // [S][R] device row addresses
-  unsigned char* buf = smem + ring_buf_offset(p.stages, p.rows);
-  const int S = p.stages, R = p.rows, SB = p.stage_bytes, tok = x.tok_bytes;
+  unsigned char* buf = smem + ring_buf_offset();
+  const int S = p.stages, SB = p.stage_bytes, tok = x.tok_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, b = blockIdx.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 32 * p.warps);   // one cp.async arrive (.noinc) per gather thread
+      mbar_init(&full[s], 32);   // one cp.async arrive (.noinc) per thread of the piece's gather warp
       mbar_init(&empty[s], 1);
     }
     mbar_init_fence();
@@ -336,29 +428,23 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
       if (p.counters && lane == 0) arrive_layer<1>(p, l);
     }
   } else {
-    // ---------------- gather warps: pages -> stage ----------------
-    const int gt = threadIdx.x - 32, ngt = p.warps * 32;
-    uint32_t q = 0;
+    // ---------------- gather warps: pages -> stage (warp wi: pieces q == wi mod W) ----------------
+    const int wi = warp - 1, W = p.warps;
     for (int l = p.l0; l < p.l1; ++l) {
       char* kb = p.kb[l];
       char* vb = p.vb[l];
+      const uint32_t q0 = static_cast<uint32_t>(l - p.l0) * static_cast<uint32_t>(mine);
+      const int32_t mfirst = static_cast<int32_t>((static_cast<uint32_t>(wi) + W - q0 % W) % W);   // q = q0 + m == wi (mod W)
       RowQueue rq;
-      rowq_init(p, rq, mine, gt, kb, vb);
-      for (int32_t m = 0; m < mine; ++m, ++q) {
+      rowq_init(p, rq, mfirst, mine, lane, kb, vb);
+      for (int32_t m = mfirst; m < mine; m += W) {
+        const uint32_t q = q0 + m;
         const int s = static_cast<int>(q % S);
         int n;
-        const RowPre cur = rowq_pop(p, rq, m, mine, gt, kb, vb, n);
+        uint64_t addr[kRowsPerLane];
+        rowq_pop(p, rq, m, mine, lane, kb, vb, addr, n);
         if (q >= static_cast<uint32_t>(S)) mbar_wait(&empty[s], ((q / S) - 1) & 1);
-        if (gt < R) table[s * R + gt] = row_addr(p, cur);
-        named_sync(1, ngt);
-        unsigned char* st = buf + static_cast<size_t>(s) * SB;
-        const uint64_t* tab = table + s * R;
-        const int nvec = n * x.vpt;
-        for (int v = gt; v < nvec; v += ngt) {
-          const int row = piece_row(p, v);
-          const int w = v - row * x.vpt;
-          cp_async16(st + v * 16, reinterpret_cast<const void*>(row_vec<CONTIG>(tab[row], w, x, x.head_stride)));
-        }
+        piece_rows<CONTIG, 1>(p, lane, n, addr, buf + static_cast<size_t>(s) * SB);
         cp_async_arrive_noinc(&full[s]);
       }
     }
@@ -367,10 +453,10 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
 
 }  // namespace
 
-int ring_header_bytes(int stages, int rows) { return ring_buf_offset(stages, rows); }
+int ring_header_bytes() { return ring_buf_offset(); }
 
 cudaError_t launch_ring(const RingParams& p, int dir, int ctas, cudaStream_t s) {
-  const int smem = ring_buf_offset(p.stages, p.rows) + p.stages * p.stage_bytes;
+  const int smem = ring_buf_offset() + p.stages * p.stage_bytes;
   const bool contig = p.x.head_stride == p.x.head_bytes || p.x.H == 1;
   const int threads = 32 * (1 + p.warps);
   if (dir == 0)

@@ -293,14 +293,17 @@ static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const
   W = std::max(1, std::min(kRingMaxWarps, W));
   const int target = std::max(1, env_int("STRATA_RING_STAGE_KB", kDefaultRingStageKB)) << 10;
   int R = std::min<int>(p->d.chunk_tokens, std::max(1, target / tok));
-  R = std::min(R, std::min(kRingMaxRows, 32 * W));
+  R = std::min(R, kRingMaxRows);
   const int sb = (R * tok + 127) / 128 * 128;
   int budget = p->tma_smem;
   const int cap_kb = env_int("STRATA_RING_SMEM_KB", 0);
   if (cap_kb > 0) budget = std::min(budget, cap_kb << 10);
   int S = std::min(kRingMaxStages, env_int("STRATA_RING_STAGES", kRingMaxStages));
-  while (S >= 2 && ring_header_bytes(S, R) + S * sb > budget) --S;
+  while (S >= 2 && ring_header_bytes() + S * sb > budget) --S;
   if (S < 2) return false;
+  // stage s belongs to device-side warp s % W (ring.cu): W divides S, W <= S
+  W = std::min(W, S);
+  S = S / W * W;
   std::memset(&rp, 0, offsetof(RingParams, pair_end));
   rp.x = xp;
   rp.rows = R;
@@ -309,7 +312,7 @@ static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const
   rp.pps = (p->d.chunk_tokens + R - 1) / R;
   rp.warps = W;
   rp.host_run = p->host_tok_stride == p->tok_bytes;
-  rp.piece_magic = xp.vpt_shift < 0 ? div_magic(xp.vpt, R * xp.vpt) : 0;
+  rp.bulk_store = dir == 0 && env_int("STRATA_RING_BULK_STORE", 0) != 0;
   for (int l = 0; l < p->d.num_layers; ++l) {
     rp.kb[l] = static_cast<char*>(p->k[l]);
     rp.vb[l] = static_cast<char*>(p->v[l]);

@@ -137,16 +137,17 @@ def test_event_ring_slot_reuse_never_fires_early(engine):
         with torch.cuda.stream(s1):
             torch.cuda._sleep(50_000_000)     # ~25 ms: op 1 starts long after ops 2..9 could
         t1 = c.pool.load(reqs[0], stream=s1, engine=engine)
-        tickets = [c.pool.load(r, stream=s2, engine=engine) for r in reqs[1:]]
-        assert tickets[-1] == t1 + 8
+        tickets = [c.pool.load(r, stream=s2, engine=engine) for r in reqs[1:8]]
         pages1 = torch.from_numpy(q.dev_pages[: ns[0]].astype(np.int64)).cuda()
         sums = []
-        with torch.cuda.stream(cons):
+        with torch.cuda.stream(cons):   # the consumer's waits are enqueued while op 1's ticket is live
             for l in range(g.L):
                 c.pool.wait_layer(t1, l, cons)
                 rows_k = c.k[l].view(g.num_pages, -1)[pages1].view(torch.int64).sum()
                 rows_v = c.v[l].view(g.num_pages, -1)[pages1].view(torch.int64).sum()
                 sums.append((rows_k, rows_v))
+        t9 = c.pool.load(reqs[8], stream=s2, engine=engine)   # reuses op 1's ring slot
+        assert t9 == t1 + 8 and tickets[-1] == t1 + 7
         torch.cuda.synchronize()
         c.check_load(0, g.L)
         p1 = q.dev_pages[: ns[0]]

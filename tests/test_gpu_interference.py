@@ -1,0 +1,105 @@
+"""NEXT-1: the interference budget of the library's default load at its default SM
+quota.  The paper's claim for its I/O kernel: "nearly 50 GB/s" with "less than 5 % and 10 % slowdown
+on prefill and decode" (§4.2, fig:interference), from as few as one or two CTAs
+(PAPER.md:258).  Method (round 1's settled "cool-down" protocol, tools/interference.py): the proxy
+alone and the proxy beside a continuous load alternate for 3 rounds, 1 s idle before every block;
+the median slowdown is compared with the budget, and the load's co-run rate with 85 % of the link.
+
+  prefill proxy  bf16 GEMMs of a Llama-3.1-8B layer for 2 x 4K tokens (tensor-core bound)
+  decode proxy   a read of 16 x 4K tokens of Llama-8B KV per layer for 32 layers (HBM bound)
+"""
+import statistics
+import time
+
+import pytest
+
+import kvgen
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2508_18572_b200 as st  # noqa: E402
+
+BUDGET = {"prefill": 0.05, "decode": 0.10}
+
+
+def _prefill():
+    M = 8192
+    shapes = [(4096, 6144), (4096, 4096), (4096, 28672), (14336, 4096)]
+    xs = {k: torch.randn(M, k, dtype=torch.bfloat16, device="cuda") for k, _ in shapes}
+    ws = [torch.randn(k, n, dtype=torch.bfloat16, device="cuda") for k, n in shapes]
+    return lambda: [torch.matmul(xs[k], w) for (k, _), w in zip(shapes, ws)]
+
+
+def _decode():
+    kv = [torch.randn(16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda") for _ in range(32)]
+    return lambda: [t.sum(dtype=torch.float32) for t in kv]
+
+
+def _time(fn, stream, reps=15):
+    evs = []
+    with torch.cuda.stream(stream):
+        fn()
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            evs.append((a, b))
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+
+@pytest.mark.parametrize("proxy", ["prefill", "decode"])
+def test_default_load_quota_meets_the_interference_budget(proxy):
+    g = kvgen.geometry("llama8b_32k")
+    q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks)
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+    try:
+        reqs = st.Requests.from_kvgen(q)
+        lo, hi = torch.cuda.Stream.priority_range()
+        io, comp = torch.cuda.Stream(priority=hi), torch.cuda.Stream(priority=lo)
+        bytes_load = 2 * g.L * 32768 * g.token_bytes
+        scratch = torch.empty(bytes_load // g.L, dtype=torch.uint8, device="cuda")
+        ts = []
+        for _ in range(8):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(io)
+            st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, scratch.numel(), io)
+            b.record(io)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        link = scratch.numel() / (statistics.median(ts[2:]) / 1e3) / 1e9
+        fn = _prefill() if proxy == "prefill" else _decode()
+        load = lambda: pool.load(reqs, stream=io)  # noqa: E731
+        load()
+        torch.cuda.synchronize()
+        alone, co, io_gbs = [], [], []
+        for _ in range(3):
+            time.sleep(1.0)
+            alone.append(_time(fn, comp))
+            n_loads = max(2, int(alone[-1] * 16 / (bytes_load / (0.9 * link) / 1e6)) + 2)
+            time.sleep(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(io)
+            for _ in range(n_loads):
+                load()
+            b.record(io)
+            co.append(_time(fn, comp))
+            b.synchronize()
+            io_gbs.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
+        slow = statistics.median(c / a_ - 1 for c, a_ in zip(co, alone))
+        rate = statistics.median(io_gbs)
+        print(f"{proxy}: slowdown {slow:+.3f} (rounds {[round(c / a_ - 1, 3) for c, a_ in zip(co, alone)]}), "
+              f"load beside it {rate:.1f} GB/s of a {link:.1f} GB/s link")
+        assert slow <= BUDGET[proxy], f"{proxy} slowdown {slow:.3f} > {BUDGET[proxy]}"
+        assert rate >= 0.85 * link, f"co-run load {rate:.1f} GB/s < 85 % of the {link:.1f} GB/s link"
+    finally:
+        pool.close()

@@ -1,0 +1,150 @@
+"""NEXT-2 consumer side: layer-wise overlapped prefill over pages that are still
+streaming in, and bubble filling.
+
+* "the GPU executor synchronizes with Cache Controller to ensure that the KV cache of certain layer is
+  available before the execution" (§4.1): FlashInfer paged prefill attention of layer l
+  runs on a consumer stream right after strata_wait_layer(ticket, l), while later layers are still
+  loading.  Its output must equal, byte for byte, the same attention over the same pages filled with
+  the ORACLE's load of the same host tier — so every layer's prefill read fully landed, correct KV.
+* Bubble filling (§4.3.3): decode work runs in the loading stall; the load keeps
+  >= 85 % of the host link while an HBM-bound decode proxy runs beside it.
+"""
+import statistics
+
+import numpy as np
+import pytest
+
+import kvgen
+import oracle
+from kvgen import Geometry
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2508_18572_b200 as st  # noqa: E402
+
+QO_HEADS = 32
+
+
+def _bf16_host(pool, g, seed):
+    """Finite bf16 KV in the host tier (attention needs real numbers)."""
+    gen = torch.Generator().manual_seed(seed)
+    vals = (torch.randn(g.host_bytes // 2, generator=gen) * 0.5).to(torch.bfloat16)
+    pool.host[: g.host_bytes] = vals.view(torch.uint8).numpy()
+
+
+@pytest.mark.parametrize("engine,P", [(st.STRATA_ENGINE_DEFAULT, 1), (st.STRATA_ENGINE_DEFAULT, 16),
+                                      (st.STRATA_ENGINE_LDG, 1)])
+def test_layerwise_prefill_over_streaming_pages_matches_oracle_kv(engine, P):
+    flashinfer = pytest.importorskip("flashinfer")
+    cached, new = 16384, 256
+    g = Geometry(L=16, H=8, D=128, e=2, P=P, C=64, num_pages=-(-20480 // P), num_chunks=320)
+    q = kvgen.make_requests(kvgen.rng_for(5), [cached], g.P, g.C, g.num_pages, g.num_chunks)
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    v = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    kr = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]   # oracle-loaded pool
+    vr = [torch.zeros(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+    try:
+        _bf16_host(pool, g, 11)
+        reqs = st.Requests.from_kvgen(q)
+        # ground truth: the oracle's load of every layer, copied into the second pool
+        for l in range(g.L):
+            ek, ev = [None] * g.L, [None] * g.L
+            ek[l], ev[l] = np.zeros(nb, np.uint8), np.zeros(nb, np.uint8)
+            oracle.load(g, pool.host[: g.host_bytes], ek, ev, q, l, l + 1)
+            kr[l].copy_(torch.from_numpy(ek[l]))
+            vr[l].copy_(torch.from_numpy(ev[l]))
+        view = lambda t: t.view(torch.bfloat16).view(g.num_pages, g.P, g.H, g.D)  # noqa: E731
+        ws = torch.empty(128 << 20, dtype=torch.uint8, device="cuda")
+        wrapper = flashinfer.BatchPrefillWithPagedKVCacheWrapper(ws, "NHD")
+        npages = int(q.dev_pages.size)
+        wrapper.plan(torch.tensor([0, new], dtype=torch.int32, device="cuda"),
+                     torch.tensor([0, npages], dtype=torch.int32, device="cuda"), reqs.dev_pages_d,
+                     torch.tensor([cached - (npages - 1) * g.P], dtype=torch.int32, device="cuda"),
+                     QO_HEADS, g.H, g.D, g.P, causal=False, q_data_type=torch.bfloat16, kv_data_type=torch.bfloat16)
+        qs = torch.randn(new, QO_HEADS, g.D, dtype=torch.bfloat16, device="cuda",
+                         generator=torch.Generator(device="cuda").manual_seed(3))
+        ref = [wrapper.run(qs, (view(kr[l]), view(vr[l]))) for l in range(g.L)]
+        torch.cuda.synchronize()
+
+        io, comp = torch.cuda.Stream(), torch.cuda.Stream()
+        with torch.cuda.stream(io):
+            torch.cuda._sleep(2_000_000)   # the consumer is already waiting when the load starts
+        t = pool.load(reqs, stream=io, engine=engine)
+        load_done = torch.cuda.Event(enable_timing=True)
+        load_done.record(io)
+        outs, first_done = [], torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(comp):
+            for l in range(g.L):
+                pool.wait_layer(t, l, comp)
+                outs.append(wrapper.run(qs, (view(k[l]), view(v[l]))))
+                if l == 0:
+                    first_done.record(comp)
+        torch.cuda.synchronize()
+        for l in range(g.L):
+            assert torch.equal(outs[l].view(torch.int16), ref[l].view(torch.int16)), f"layer {l} prefill differs"
+            assert torch.isfinite(outs[l].float()).all()
+        # layer 0's prefill finished while later layers were still streaming in
+        assert first_done.elapsed_time(load_done) > 0.0
+    finally:
+        pool.close()
+
+
+def test_bubble_fill_keeps_the_link_busy():
+    """A decode proxy (HBM read of 16 x 4K tokens of KV per layer, replayed from a CUDA graph) runs
+    in the load's stall; the default-engine load keeps >= 85 % of the measured contiguous link."""
+    g = kvgen.geometry("llama8b_32k")
+    q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks)
+    nb = g.num_pages * g.P * g.token_bytes
+    k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+    pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+    try:
+        reqs = st.Requests.from_kvgen(q)
+        lo, hi = torch.cuda.Stream.priority_range()
+        io, dec = torch.cuda.Stream(priority=hi), torch.cuda.Stream(priority=lo)
+        bytes_load = 2 * g.L * 32768 * g.token_bytes
+        scratch = torch.empty(bytes_load // g.L, dtype=torch.uint8, device="cuda")
+        ts = []
+        for _ in range(8):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(io)
+            st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, scratch.numel(), io)
+            b.record(io)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        link = scratch.numel() / (statistics.median(ts[2:]) / 1e3) / 1e9
+        kv = torch.randn(16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda")
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(dec):
+            kv.sum(dtype=torch.float32)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gr, stream=dec):
+                for _ in range(8):
+                    kv.sum(dtype=torch.float32)
+        pool.load(reqs, stream=io)
+        torch.cuda.synchronize()
+        # decode steps queued for longer than the loads take
+        with torch.cuda.stream(dec):
+            for _ in range(60):
+                gr.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(io)
+        for _ in range(3):
+            pool.load(reqs, stream=io)
+        b.record(io)
+        b.synchronize()
+        dec_busy = not dec.query()
+        torch.cuda.synchronize()
+        gbs = 3 * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
+        assert dec_busy, "the decode proxy finished before the loads: no co-run"
+        assert gbs >= 0.85 * link, f"load {gbs:.1f} GB/s beside decode < 85 % of the {link:.1f} GB/s link"
+    finally:
+        pool.close()

@@ -205,3 +205,44 @@ def test_shared_tier_across_ranks_gloo(tmp_path):
         assert p.exitcode == 0
     assert q.get(timeout=10), "head slices of the shared tier do not reassemble the full-head load"
     assert not os.path.exists(path), "creator did not unlink the shared tier"
+
+
+def _bench_reduce_worker(rank, world, port, out_q):
+    """bench.py's own multi-rank reduction and reporting code (reduce_max, gather_floats,
+    scale_record) under gloo: rank r took (1 + r) s for its steps and saw a link of (50 + r) GB/s."""
+    import sys
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        cv_max = bench.reduce_max(dist, world, 0.01 * (rank + 1))
+        per_rank = bench.gather_floats(dist, world, [1.0 + rank, 50.0 + rank])
+        rec = bench.scale_record(per_rank, bytes_per_step_per_rank=10 ** 9, steps=10)
+        if rank == 0:
+            out_q.put((cv_max, per_rank, rec))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_reductions_gloo():
+    """Weak-scaling aggregate = all ranks' bytes over the SLOWEST rank's time; each rank's fraction is
+    of its OWN concurrently measured link; the line reports the minimum."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_reduce_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=180)
+        assert p.exitcode == 0
+    cv_max, per_rank, rec = q.get(timeout=10)
+    assert cv_max == pytest.approx(0.02)
+    assert per_rank == [[1.0, 50.0], [2.0, 51.0]]
+    assert rec["value"] == pytest.approx(2 * 10 * 1e9 / 2.0 / 1e9)       # 10 GB/s over the max time
+    assert rec["per_rank_gbs"] == [10.0, 5.0]
+    assert rec["per_rank_frac_of_link"] == [round(10.0 / 50.0, 4), round(5.0 / 51.0, 4)]
+    assert rec["min_frac_over_ranks"] == round(5.0 / 51.0, 4)

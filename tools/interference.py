@@ -103,6 +103,10 @@ def main():
     ap.add_argument("--engines", default="1,2")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--groups", default="0", help="DMA layer_group values (engine 4 only)")
+    ap.add_argument("--ring-smem", default="0",
+                    help="ring engine (engine 2) shared-memory budgets per CTA in KiB (0 = all): bounds the host "
+                         "bytes in flight (STRATA_RING_SMEM_KB)")
+    ap.add_argument("--ring-stage", default="0", help="ring engine piece sizes in KiB (0 = default; STRATA_RING_STAGE_KB)")
     ap.add_argument("--memcpy", type=int, default=0, help="also co-run a contiguous cudaMemcpyAsync loop (-1 engine)")
     ap.add_argument("--cooldown", type=float, default=1.0,
                     help="idle seconds before every alone / co-run block (power-state reset for the GEMM proxy)")
@@ -140,7 +144,10 @@ def main():
 
     scratch = torch.empty(bytes_load // g.L, dtype=torch.uint8, device="cuda")
 
-    def make_io(eng, c, G):
+    def make_io(eng, c, G, env):
+        for key in ("STRATA_RING_SMEM_KB", "STRATA_RING_STAGE_KB"):
+            os.environ.pop(key, None)
+        os.environ.update(env)
         if eng < 0:   # contiguous memcpy of the same bytes: 32 copies of one layer's worth
             def run():
                 for _ in range(g.L):
@@ -152,12 +159,18 @@ def main():
     for eng in [int(x) for x in args.engines.split(",")]:
         for c in [int(x) for x in args.ctas.split(",")]:
             for G in ([int(x) for x in args.groups.split(",")] if eng == 4 else [0]):
-                configs.append((eng, c, G))
+                envs = [{}]
+                if eng == 2:
+                    envs = [{**({"STRATA_RING_SMEM_KB": str(m)} if int(m) else {}),
+                             **({"STRATA_RING_STAGE_KB": str(k_)} if int(k_) else {})}
+                            for m in args.ring_smem.split(",") for k_ in args.ring_stage.split(",")]
+                for env in envs:
+                    configs.append((eng, c, G, env))
     if args.memcpy:
-        configs.append((-1, 0, 0))
-    for eng, c, G in configs:
+        configs.append((-1, 0, 0, {}))
+    for eng, c, G, env in configs:
         if True:
-            load = make_io(eng, c, G)
+            load = make_io(eng, c, G, env)
             # I/O alone
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             load()
@@ -193,6 +206,7 @@ def main():
                     io_cos.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
                 al, co = statistics.median(alone_ms), statistics.median(co_ms)
                 print(json.dumps({"kind": "corun", "graph": args.graph, "engine": eng, "ctas": c, "layer_group": G,
+                                  "env": env,
                                   "proxy": name, "proxy_alone_ms": round(al, 4), "proxy_corun_ms": round(co, 4),
                                   "slowdown": round(co / al - 1, 4),
                                   "slowdown_rounds": [round(x / y - 1, 4) for x, y in zip(co_ms, alone_ms)],

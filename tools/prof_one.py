@@ -37,6 +37,7 @@ def main():
     pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
                        k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=g.num_pages, num_chunks=g.num_chunks,
                        host_heads=g.Ht, head_begin=g.h0, head_major=g.head_major)
+    kvgen.fill_random(pool.host, 3)
     reqs = st.Requests.from_kvgen(q)
     fn = pool.load if args.dir == "h2d" else pool.offload
     for _ in range(args.reps):

@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--frag", default="perm", help="page table: perm | identity | churn")
     ap.add_argument("--chunk-frag", default="perm", help="host chunk order: perm | identity")
     ap.add_argument("--tag", default="")
+    ap.add_argument("--bulk-store", default="0", help="load: 0 st.global scatter, 1 cp.async.bulk stores (list)")
     args = ap.parse_args()
     io = torch.cuda.Stream()
     for spec in args.configs.split(","):
@@ -79,8 +80,11 @@ def main():
         for d in args.dirs.split(","):
             for c in [int(x) for x in args.ctas.split(",")]:
                 for w in [int(x) for x in (args.warps if d == "load" else args.gather_warps).split(",")]:
-                    for skb in [int(x) for x in args.stage_kb.split(",")]:
+                    for skb, bs in [(a_, b_) for a_ in args.stage_kb.split(",")
+                                    for b_ in (args.bulk_store.split(",") if d == "load" else ["0"])]:
+                        skb = int(skb)
                         os.environ["STRATA_RING_STAGE_KB"] = str(skb)
+                        os.environ["STRATA_RING_BULK_STORE"] = bs
                         os.environ["STRATA_RING_WARPS" if d == "load" else "STRATA_RING_GATHER_WARPS"] = str(w)
                         if d == "load":
                             for l in check_layers:
@@ -99,10 +103,10 @@ def main():
                             ok = bool((pool.host == host_ref).all())   # loaded from this tier: offload rewrites the same bytes
                         print(json.dumps({"kind": "ring", "tag": args.tag, "flags": args.flags, "frag": args.frag,
                                           "chunk_frag": args.chunk_frag, "config": name, "P": g.P, "dir": d, "ctas": c, "warps": w,
-                                          "stage_kb": skb, "gbs": round(r, 2),
+                                          "stage_kb": skb, "bulk_store": int(bs), "gbs": round(r, 2),
                                           "frac_link": round(r / (link if d == "load" else link_d2h), 4),
                                           "parity": ok}), flush=True)
-        for key in ("STRATA_RING_STAGE_KB", "STRATA_RING_WARPS", "STRATA_RING_GATHER_WARPS"):
+        for key in ("STRATA_RING_STAGE_KB", "STRATA_RING_WARPS", "STRATA_RING_GATHER_WARPS", "STRATA_RING_BULK_STORE"):
             os.environ.pop(key, None)
         pool.close()
         del k, v
