@@ -49,7 +49,13 @@
  *
  * ENVIRONMENT (defaults are the measured choices of DESIGN.md §6; the knobs exist for A/B runs):
  *   STRATA_VALIDATE=1          as the STRATA_VALIDATE pool flag, for every pool
- *   STRATA_LDG_FUSED=0|force   per-layer LDG launches only | fuse even 1-CTA grids (default: fuse >= 2)
+ *   STRATA_RING_INFLIGHT_KB=n  ring: host bytes in flight over all CTAs, KiB (default 224)
+ *   STRATA_RING_STAGE_KB=n     ring: piece size (default 16)
+ *   STRATA_RING_WARPS=n        ring: scatter warps per load CTA (default 8; STRATA_RING_GATHER_WARPS for offloads, 4)
+ *   STRATA_RING_SMEM_KB=n      ring: cap on a CTA's shared memory
+ *   STRATA_RING_EXCLUSIVE=1    ring: a CTA reserves its SM's shared memory (no co-resident CTAs)
+ *   STRATA_RING_BULK_STORE=1   ring loads: page writes as cp.async.bulk stores instead of st.global
+ *   STRATA_LDG_FUSED=0|force   per-layer launches only (LDG and ring) | fuse even 1-CTA LDG grids
  *   STRATA_COPY_STREAMS=n      copy streams of the DMA engine per direction (default 1)
  *   STRATA_STAGE_MB=n          DMA staging slot size (default 128)
  *   STRATA_DMA_EDGE_SPLIT=n    first / last layer in n times smaller pieces (default 4; 1 = off)
@@ -111,12 +117,15 @@ enum strata_pool_flags {
 
 /* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
 enum strata_engine {
-  STRATA_ENGINE_DEFAULT = 0,  /* library choice (B200 measurements): STRATA_ENGINE_DMA when
-                                 host_chunks_host is given and a layer moves >= 4 MiB (offloads then
-                                 group layers into >= 128 KiB runs, see layer_group), else LDG */
+  STRATA_ENGINE_DEFAULT = 0,  /* library choice: a zero-copy kernel — STRATA_ENGINE_TMA (the ring)
+                                 wherever the tier has whole host rows in 16-byte units (and for
+                                 loads of 8- / 4-byte-granular narrow rows), else STRATA_ENGINE_LDG.
+                                 The copy engines (DMA) run only when asked for. */
   STRATA_ENGINE_LDG = 1,      /* warps, 16-byte LDG/STG register staging, warp index broadcast */
-  STRATA_ENGINE_TMA = 2,      /* load: one cp.async.bulk producer warp + 15 LSU consumer warps per CTA
-                                 over a shared-memory ring; offload: as STRATA_ENGINE_TMA_BULK */
+  STRATA_ENGINE_TMA = 2,      /* the ring engine: one persistent launch per operation; per CTA a TMA
+                                 warp moves each page-first host run (<= 16 KiB piece) with one
+                                 cp.async.bulk through a shared-memory ring, LSU warps scatter the
+                                 rows to their pages (offload: cp.async gather, bulk host store) */
   STRATA_ENGINE_TMA_BULK = 3, /* one warp per CTA, cp.async.bulk on both sides of the ring */
   STRATA_ENGINE_DMA = 4       /* copy-engine gather of whole page-first host runs (cudaMemcpyBatchAsync,
                                  one in-order copy stream) into a double-buffered HBM staging ring + the LDG
@@ -143,8 +152,7 @@ typedef struct {
   void* host_base;                /* caller host memory to register, or NULL: library allocates */
   int64_t num_chunks;             /* host capacity in chunks (>= 1) */
   int32_t host_heads;             /* Ht: heads per token in the host tier (0 = num_heads) */
-  int32_t head_begin;             /* h0: first host head this GPU moves; h0 + num_heads <= Ht.
-                                     With Ht > num_heads or head-major chunks, D*e % 16 == 0. */
+  int32_t head_begin;             /* h0: first host head this GPU moves; h0 + num_heads <= Ht */
 } strata_pool_desc;
 
 typedef struct {
@@ -152,8 +160,8 @@ typedef struct {
   int32_t layer_begin;            /* l0, half-open layer range [l0, l1) (R11) */
   int32_t layer_end;              /* l1, 0 <= l0 <= l1 <= L */
   int32_t engine;                 /* strata_engine */
-  int32_t num_ctas;               /* SM quota; 0 = library default (LDG: 2 CTAs
-                                     for loads, 1 for offloads — the paper's quotas) */
+  int32_t num_ctas;               /* SM quota; 0 = library default (ring: 2 CTAs,
+                                     4 for rows < 1 KiB; LDG: 2 for loads, 1 for offloads) */
   int32_t threads;                /* threads per CTA for STRATA_ENGINE_LDG; 0 = default */
   const int64_t* num_tokens;      /* [R] host: tokens to move per request (>= 0) */
   const int32_t* host_chunks;     /* device int32: all requests' chunk lists concatenated */
@@ -171,14 +179,20 @@ typedef struct {
                                      run (page-first chunks keep them contiguous).  Layer l's event
                                      then completes with its group [l0 + G*k, l0 + G*(k+1)), i.e.
                                      coarser overlap for larger copies.  0 or 1 = per layer. */
-  int32_t reserved;
+  int32_t inflight_kib;           /* ring engine: host bytes kept in flight over all CTAs, in KiB
+                                     (0 = library default, 224).  The interference knob of
+                                     PAPER.md:257-262 beside num_ctas: co-running HBM-bound work slows
+                                     with the host reads queued, not with the SMs used.
+                                     Ignored by the other engines. */
 } strata_xfer;
 
 /* Register the host tier and bind it to the device pool described by *d ("CPU registered pinned
  * memory" the I/O kernels read directly, §4.2; a node-sized pinned tier).
- * Host memory: if d->host_base != NULL it must hold num_chunks*chunk_bytes bytes, 16-byte aligned;
- * the library page-locks and maps it (cudaHostRegisterMapped|Portable) and unregisters it in
- * strata_unregister_host_pool; the caller keeps ownership.  If NULL, the library allocates it
+ * Host memory: if d->host_base != NULL it must hold num_chunks*chunk_bytes bytes, aligned to the
+ * element size; the library page-locks and maps it (cudaHostRegisterMapped|Portable) and
+ * unregisters it when the LAST pool whose tier lies inside that registration closes (several pools
+ * — e.g. the TP ranks of one process — may share one caller tier); memory the caller registered
+ * itself is never unregistered by the library; the caller keeps ownership.  If NULL, the library allocates it
  * (NUMA-local to the GPU, pre-touched, optionally huge pages / write-combined), owns and frees it.
  * Device buffers stay caller-owned and must outlive the handle.
  * Errors: INVALID_ARG, ALIGNMENT, OOM, CUDA.  On error *out is set to NULL. */
@@ -212,7 +226,11 @@ int strata_offload(strata_pool_t p, const strata_xfer* x, strata_stream_t stream
  * of operation `ticket` (0 = the latest operation).  The event stays valid until the ring slot is
  * reused 8 operations later; an older ticket returns STRATA_ERR_STALE_TICKET.  A layer outside the
  * operation's range returns STRATA_ERR_INVALID_ARG.  Use with cudaStreamWaitEvent /
- * cudaEventSynchronize; never destroy it. */
+ * cudaEventSynchronize; never destroy it.  An operation issued while its stream was being captured
+ * into a CUDA graph has its events inside that graph only: wait on them from the same capture;
+ * strata_layer_elapsed_ms on such a ticket returns STRATA_ERR_UNSUPPORTED.  A new operation that
+ * reuses a ring slot is ordered after the slot's previous one-launch operation (whose device-side
+ * layer flags it shares), so a layer event never fires before that layer's bytes landed. */
 int strata_layer_event(strata_pool_t p, uint64_t ticket, int32_t layer, strata_event_t* out);
 
 /* Consumer-side wait: make stream `consumer` wait until layer `layer` of operation

@@ -168,7 +168,7 @@ class Requests:
         return int(self.num_tokens.sum())
 
     def xfer(self, layer_begin: int, layer_end: int, engine: int = 0, num_ctas: int = 0, threads: int = 0,
-             host_lists: bool = False, layer_group: int = 0) -> Xfer:
+             host_lists: bool = False, layer_group: int = 0, inflight_kib: int = 0) -> Xfer:
         """strata_xfer pointing at these tables (device lists, or host lists for the baselines)."""
         hc = self.host_chunks_h.ctypes.data if host_lists else self.host_chunks_d.data_ptr()
         dp = self.dev_pages_h.ctypes.data if host_lists else self.dev_pages_d.data_ptr()
@@ -178,7 +178,7 @@ class Requests:
                     page_start=self.page_start.ctypes.data, chunk_offset=self.chunk_offset.ctypes.data,
                     page_offset=self.page_offset.ctypes.data, host_chunks_len=self.host_chunks_h.size,
                     dev_pages_len=self.dev_pages_h.size, host_chunks_host=self.host_chunks_h.ctypes.data,
-                    layer_group=layer_group)
+                    layer_group=layer_group, inflight_kib=inflight_kib)
 
 
 class HostPool:
@@ -240,16 +240,17 @@ class HostPool:
             pass
 
     def _op(self, fn, name: str, reqs: Requests, layer_begin: int, layer_end: Optional[int], stream, engine: int,
-            num_ctas: int, threads: int, layer_group: int) -> int:
+            num_ctas: int, threads: int, layer_group: int, inflight_kib: int = 0) -> int:
         # The strata_xfer of a (Requests, layer range, options) tuple is built once and reused: its
         # pointers are those of the Requests' arrays, which stay put, while the C call re-reads the
         # values behind them (num_tokens, offsets) every time.  Saves ~15 us of ctypes marshalling
         # per call, which is most of a small load's host cost.
         key = (layer_begin, self.num_layers if layer_end is None else layer_end, engine, num_ctas, threads,
-               layer_group)
+               layer_group, inflight_kib)
         x = reqs._xcache.get(key)
         if x is None:
-            x = reqs._xcache[key] = reqs.xfer(key[0], key[1], engine, num_ctas, threads, layer_group=layer_group)
+            x = reqs._xcache[key] = reqs.xfer(key[0], key[1], engine, num_ctas, threads, layer_group=layer_group,
+                                              inflight_kib=inflight_kib)
         check(fn(self._hptr, ctypes.byref(x), ctypes.c_void_p(_stream_handle(stream)), self._ticket), name)
         if stream is not None and hasattr(stream, "cuda_stream"):
             # the kernels read the device index lists on `stream`: keep torch's caching allocator
@@ -259,14 +260,15 @@ class HostPool:
         return self._ticket.value
 
     def load(self, reqs: Requests, layer_begin: int = 0, layer_end: Optional[int] = None, stream=None,
-             engine: int = 0, num_ctas: int = 0, threads: int = 0, layer_group: int = 0) -> int:
+             engine: int = 0, num_ctas: int = 0, threads: int = 0, layer_group: int = 0, inflight_kib: int = 0) -> int:
         return self._op(_lib.lib().strata_load, "strata_load", reqs, layer_begin, layer_end, stream, engine,
-                        num_ctas, threads, layer_group)
+                        num_ctas, threads, layer_group, inflight_kib)
 
     def offload(self, reqs: Requests, layer_begin: int = 0, layer_end: Optional[int] = None, stream=None,
-                engine: int = 0, num_ctas: int = 0, threads: int = 0, layer_group: int = 0) -> int:
+                engine: int = 0, num_ctas: int = 0, threads: int = 0, layer_group: int = 0,
+                inflight_kib: int = 0) -> int:
         return self._op(_lib.lib().strata_offload, "strata_offload", reqs, layer_begin, layer_end, stream, engine,
-                        num_ctas, threads, layer_group)
+                        num_ctas, threads, layer_group, inflight_kib)
 
     def layer_event(self, ticket: int, layer: int) -> int:
         return strata_layer_event(self.handle, ticket, layer)

@@ -78,7 +78,7 @@ class Xfer(ctypes.Structure):
         ("num_tokens", ctypes.c_void_p), ("host_chunks", ctypes.c_void_p), ("chunk_start", ctypes.c_void_p),
         ("dev_pages", ctypes.c_void_p), ("page_start", ctypes.c_void_p), ("chunk_offset", ctypes.c_void_p),
         ("page_offset", ctypes.c_void_p), ("host_chunks_len", ctypes.c_int64), ("dev_pages_len", ctypes.c_int64),
-        ("host_chunks_host", ctypes.c_void_p), ("layer_group", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("host_chunks_host", ctypes.c_void_p), ("layer_group", ctypes.c_int32), ("inflight_kib", ctypes.c_int32),
     ]
 
 

@@ -118,6 +118,9 @@ struct RingParams {
   int32_t host_run;             // 1: a piece's host rows are one contiguous run (host_tok_stride == tok)
   int32_t warps;                // device-side LSU warps per CTA: load scatter / offload gather (+1 TMA warp)
   int32_t bulk_store;           // load: the device side as cp.async.bulk stores instead of st.global
+  int32_t smem_reserve;         // > 0: dynamic shared memory to request (>= the ring's): keeps the SM exclusive
+  uint32_t word_magic;          // narrow rows: row of word v < R*tok/gran = umulhi(v, magic) (0: divide)
+  int32_t debug;                // A/B experiments only (env STRATA_RING_DEBUG): bit 0 = skip the page writes
   int32_t pair_end[kMaxReqsPerLaunch];   // inclusive prefix sums of chunk positions per request
   char* kb[kMaxFusedLayers];    // per-layer K / V bases
   char* vb[kMaxFusedLayers];
@@ -263,11 +266,20 @@ constexpr int kDefaultUnroll = 8;
 constexpr int kDefaultCtasTma = 2;   // STRATA_ENGINE_TMA_BULK (scaled up for small rows, transfer.cpp)
 // The ring engine (ring.cu), the default.  Loads: CTAs of 1 producer + kDefaultRingWarps scatter
 // warps; offloads: CTAs of 1 gather + 1 store warp; 32 KiB pieces, as many stages as fit.
+// Quotas (profiles/r02/ring_sweep6_bulkstore_70b.jsonl, ring_sweep5_warp_pieces.jsonl): rows of >= 1 KiB
+// reach the SM zero-copy plateau (51.4 GB/s load, 52.6 offload) from 2 CTAs, 256-byte rows (70B TP=8)
+// need 4 (2 CTAs: 43.8 / 40.1).  One CTA tops out at ~36-39 GB/s: the SM's L1->XBAR request path
+// (profiles/r02/ncu_ring_load_1cta_v4.txt).
 constexpr int kDefaultCtasRingLoad = 2;
-constexpr int kDefaultCtasRingOffload = 1;
+constexpr int kDefaultCtasRingOffload = 2;
+constexpr int kRingSmallRowBytes = 1024;   // rows below this take twice the quota
+constexpr int64_t kSmallOpBytes = int64_t(16) << 20;   // ring operations below this: all pieces in flight
+constexpr int kSmallOpCtas = 16;
 constexpr int kDefaultRingWarps = 8;         // load: scatter warps
-constexpr int kDefaultRingGatherWarps = 4;   // offload: cp.async gather warps
-constexpr int kDefaultRingStageKB = 32;
+constexpr int kDefaultRingGatherWarps = 8;   // offload: cp.async gather warps
+constexpr int kDefaultRingStageKB = 16;
+constexpr int kDefaultRingInflightKB = 224;  // host bytes in flight over all CTAs (2 CTAs: 7 x 16 KiB each)
+constexpr int kDefaultRingExclusive = 0;     // 1: a ring CTA reserves its SM's shared memory
 constexpr int kTmaStageTarget = 32 << 10;
 
 int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan);                     // transfer.cpp

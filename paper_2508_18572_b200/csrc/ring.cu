@@ -34,10 +34,10 @@ namespace {
 
 using namespace dev;
 
-constexpr int kRingBarBytes = 2 * kRingMaxStages * 8;   // full[16], empty[16]
+constexpr int kRingBarBytes = 2 * kRingMaxStages * 8 + kRingMaxStages * 4;   // full[16], empty[16], pad[16]
 constexpr int kU = 4;                                   // 16-byte vectors in flight per scatter lane
 
-// [full[16] | empty[16] | pad to 128 | S stages]
+// [full[16] | empty[16] | pad[16] (narrow rows: host-run offset in its 16-byte unit) | pad to 128 | S stages]
 __host__ __device__ constexpr int ring_buf_offset() { return (kRingBarBytes + 127) / 128 * 128; }
 
 struct Piece {
@@ -160,13 +160,17 @@ __device__ __forceinline__ void rowq_pop(const RingParams& p, RowQueue& q, int32
   rowq_set(p, q, kLook - 1, m + kLook * p.warps, mine, lane, kb, vb);
 }
 
-// Row j's device address, held by lane j % 32 in slot j / 32.
+// Row j's device address, held by lane j % 32 in slot j / 32.  Lanes may ask for rows of different
+// slots in one instruction (narrow rows whose vector count is not a power of two: a group of 32 / vpt
+// rows can straddle row 32), so every slot is shuffled and the lane keeps its own.
 __device__ __forceinline__ uint64_t row_base(const uint64_t (&addr)[kRowsPerLane], int j) {
-  uint64_t v = addr[0];
+  uint64_t v = 0;
 #pragma unroll
-  for (int c = 1; c < kRowsPerLane; ++c)
-    if ((j >> 5) == c) v = addr[c];
-  return __shfl_sync(kFull, v, j & 31);
+  for (int c = 0; c < kRowsPerLane; ++c) {
+    const uint64_t t = __shfl_sync(kFull, addr[c], j & 31);
+    if ((j >> 5) == c) v = t;
+  }
+  return v;
 }
 
 // Every (row, 16-byte vector) of one piece by one warp.  Wide rows (vpt >= 32): one row at a time,
@@ -266,12 +270,46 @@ __device__ __forceinline__ void piece_rows_bulk(const RingParams& p, int lane, i
 }
 
 // ---------------------------------------------------------------------------------------------
-template <bool CONTIG>
+// Narrow rows (R29: a pool whose rows, strides or bases are multiples of 8 or 4 bytes but not 16):
+// the host run of a piece starts `pad` = src % 16 bytes into a 16-byte unit, so the producer copies
+// the enclosing 16-byte-aligned span (a few bytes of the neighbouring rows of the same tier ride
+// along, never written anywhere) and records `pad` for the stage; the scatter moves WORD-byte words.
+template <int WORD>
+struct WordT;
+template <> struct WordT<8> { using T = unsigned long long; };
+template <> struct WordT<4> { using T = unsigned int; };
+
+template <int WORD>
+__device__ __forceinline__ void piece_rows_narrow(const RingParams& p, int lane, int n,
+                                                  const uint64_t (&addr)[kRowsPerLane], const unsigned char* st) {
+  using T = typename WordT<WORD>::T;
+  const int tok = p.x.tok_bytes, wpr = tok / WORD;
+  const int total = n * wpr;
+  for (int v0 = 0; v0 < total; v0 += 32 * kU) {
+    T val[kU];
+    uint64_t dst[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int v = v0 + u * 32 + lane;
+      const int j = p.word_magic ? static_cast<int>(__umulhi(static_cast<unsigned>(v), p.word_magic)) : v / wpr;
+      const int w = v - j * wpr;
+      const uint64_t base = row_base(addr, j & (kRingMaxRows - 1));   // every lane shuffles (convergent)
+      dst[u] = base + static_cast<uint64_t>(w) * WORD;
+      if (v < total) val[u] = *reinterpret_cast<const T*>(st + j * tok + w * WORD);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (v0 + u * 32 + lane < total) *reinterpret_cast<T*>(dst[u]) = val[u];
+  }
+}
+
+template <bool CONTIG, int WORD>
 __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(const __grid_constant__ RingParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const XferParams& x = p.x;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kRingMaxStages;
+  int* pads = reinterpret_cast<int*>(empty + kRingMaxStages);
   unsigned char* buf = smem + ring_buf_offset();
   const int S = p.stages, SB = p.stage_bytes, tok = x.tok_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -307,9 +345,22 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(
           const uint64_t a = __shfl_sync(kFull, reinterpret_cast<uint64_t>(src), t);
           const int nt = __shfl_sync(kFull, n, t);
           if (q >= static_cast<uint32_t>(S)) mbar_wait(&empty[s], ((q / S) - 1) & 1);
+          unsigned char* st = buf + static_cast<size_t>(s) * SB;
+          if (WORD < 16) {
+            // the enclosing 16-byte-aligned span of the run; the stage's rows start `pad` bytes in
+            const uint64_t a0 = a & ~uint64_t(15);
+            const uint32_t pad = static_cast<uint32_t>(a - a0);
+            const uint32_t span = nt ? (pad + static_cast<uint32_t>(nt * tok) + 15u) & ~15u : 0u;
+            if (lane == 0) {
+              pads[s] = static_cast<int>(pad);
+              mbar_arrive_expect_tx(&full[s], span);   // releases the pad write to the stage's scatter warp
+              if (span) bulk_g2s(st, reinterpret_cast<const void*>(a0), span, &full[s]);
+            }
+            __syncwarp();
+            continue;
+          }
           if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nt * tok));
           __syncwarp();
-          unsigned char* st = buf + static_cast<size_t>(s) * SB;
           if (p.host_run) {
             if (lane == 0 && nt) bulk_g2s(st, reinterpret_cast<const void*>(a), static_cast<uint32_t>(nt * tok), &full[s]);
           } else {
@@ -337,7 +388,11 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(
         uint64_t addr[kRowsPerLane];
         rowq_pop(p, rq, m, mine, lane, kb, vb, addr, n);
         mbar_wait(&full[s], (q / S) & 1);
-        if (p.bulk_store) {
+        if (WORD < 16) {
+          piece_rows_narrow<WORD < 16 ? WORD : 8>(p, lane, n, addr, buf + static_cast<size_t>(s) * SB + pads[s]);
+        } else if (p.debug & 1) {
+          // A/B only (STRATA_RING_DEBUG=1): the host reads without the page writes
+        } else if (p.bulk_store) {
           piece_rows_bulk<CONTIG>(p, lane, n, addr, buf + static_cast<size_t>(s) * SB);
           bulk_wait_read<0>();   // the TMA has read this stage
         } else {
@@ -456,20 +511,26 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
 int ring_header_bytes() { return ring_buf_offset(); }
 
 cudaError_t launch_ring(const RingParams& p, int dir, int ctas, cudaStream_t s) {
-  const int smem = ring_buf_offset() + p.stages * p.stage_bytes;
+  // exclusive: reserve the SM's shared memory so no other kernel's CTA shares the SM
+  const int smem = p.smem_reserve > 0 ? p.smem_reserve : ring_buf_offset() + p.stages * p.stage_bytes;
   const bool contig = p.x.head_stride == p.x.head_bytes || p.x.H == 1;
   const int threads = 32 * (1 + p.warps);
-  if (dir == 0)
-    return contig ? launch_k(ring_load_kernel<true>, ctas, threads, smem, s, p)
-                  : launch_k(ring_load_kernel<false>, ctas, threads, smem, s, p);
+  if (dir == 0) {
+    if (p.x.gran == 8) return launch_k(ring_load_kernel<true, 8>, ctas, threads, smem, s, p);
+    if (p.x.gran == 4) return launch_k(ring_load_kernel<true, 4>, ctas, threads, smem, s, p);
+    return contig ? launch_k(ring_load_kernel<true, 16>, ctas, threads, smem, s, p)
+                  : launch_k(ring_load_kernel<false, 16>, ctas, threads, smem, s, p);
+  }
   return contig ? launch_k(ring_offload_kernel<true>, ctas, threads, smem, s, p)
                 : launch_k(ring_offload_kernel<false>, ctas, threads, smem, s, p);
 }
 
 cudaError_t ring_prepare(int smem) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(ring_load_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(ring_load_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(ring_load_kernel<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(ring_load_kernel<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(ring_load_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
+  if ((e = cudaFuncSetAttribute(ring_load_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(ring_offload_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   return cudaFuncSetAttribute(ring_offload_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }

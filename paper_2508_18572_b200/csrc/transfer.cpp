@@ -280,12 +280,22 @@ static int env_int(const char* name, int def) {
 }
 
 // The ring engine needs whole host token rows (token-major tiers, or one head per GPU) in 16-byte
-// units; a head-major tier with several heads per GPU has no whole rows.
-static bool ring_supported(const strata_pool* p) { return p->gran == 16 && p->host_row_contig(); }
+// units; a head-major tier with several heads per GPU has no whole rows.  Loads of narrow rows (R29,
+// 8- or 4-byte granularity) take it too when a piece's host rows are one run, the device rows are
+// head-contiguous and the tier's mapping spans whole 16-byte units (the producer reads the enclosing
+// aligned span of each run).
+static bool ring_supported(const strata_pool* p, int dir) {
+  if (!p->host_row_contig()) return false;
+  if (p->gran == 16) return true;
+  return dir == 0 && (p->gran == 8 || p->gran == 4) && p->host_tok_stride == p->tok_bytes &&
+         (p->head_stride == p->head_bytes || p->d.num_heads == 1) &&
+         reinterpret_cast<uintptr_t>(p->host_dev) % 16 == 0 && p->host_bytes % 16 == 0;
+}
 
 // Ring geometry for this pool and direction (rows per piece, stages, scatter warps); false when a
 // 2-stage ring of one-row pieces does not fit in shared memory.
-static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const XferParams& xp, RingParams& rp) {
+static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const XferParams& xp, int ctas,
+                      RingParams& rp) {
   const int tok = static_cast<int>(p->tok_bytes);
   int W = x->threads ? x->threads / 32 - 1
                      : dir == 0 ? env_int("STRATA_RING_WARPS", kDefaultRingWarps)
@@ -294,16 +304,27 @@ static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const
   const int target = std::max(1, env_int("STRATA_RING_STAGE_KB", kDefaultRingStageKB)) << 10;
   int R = std::min<int>(p->d.chunk_tokens, std::max(1, target / tok));
   R = std::min(R, kRingMaxRows);
-  const int sb = (R * tok + 127) / 128 * 128;
+  // narrow rows: the stage holds the run's enclosing 16-byte-aligned span (up to 30 bytes more)
+  const int sb = (R * tok + (p->gran < 16 ? 32 : 0) + 127) / 128 * 128;
   int budget = p->tma_smem;
   const int cap_kb = env_int("STRATA_RING_SMEM_KB", 0);
   if (cap_kb > 0) budget = std::min(budget, cap_kb << 10);
-  int S = std::min(kRingMaxStages, env_int("STRATA_RING_STAGES", kRingMaxStages));
+  // host bytes kept in flight (the rings' capacity) over all CTAs: the caller's bound
+  // (strata_xfer.inflight_kib), else the default — the knee of the throughput / interference
+  // frontier: more than the link needs only queues requests, and queued host reads
+  // are what slows co-running HBM-bound work
+  const int64_t total = x->inflight_kib > 0 ? x->inflight_kib : env_int("STRATA_RING_INFLIGHT_KB", kDefaultRingInflightKB);
+  const int64_t per_cta = (total << 10) / std::max(1, ctas);
+  int S = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(kRingMaxStages, per_cta / sb)));
+  S = std::min(S, env_int("STRATA_RING_STAGES", kRingMaxStages));
   while (S >= 2 && ring_header_bytes() + S * sb > budget) --S;
   if (S < 2) return false;
-  // stage s belongs to device-side warp s % W (ring.cu): W divides S, W <= S
-  W = std::min(W, S);
-  S = S / W * W;
+  // stage s belongs to device-side warp s % W (ring.cu), so W must divide S: the ring capacity S
+  // (the host bytes in flight) is kept and W becomes the largest divisor of S not above the request
+  int Wd = 1;
+  for (int d = 1; d <= std::min(W, S); ++d)
+    if (S % d == 0) Wd = d;
+  W = Wd;
   std::memset(&rp, 0, offsetof(RingParams, pair_end));
   rp.x = xp;
   rp.rows = R;
@@ -313,6 +334,9 @@ static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const
   rp.warps = W;
   rp.host_run = p->host_tok_stride == p->tok_bytes;
   rp.bulk_store = dir == 0 && env_int("STRATA_RING_BULK_STORE", 0) != 0;
+  rp.debug = env_int("STRATA_RING_DEBUG", 0);
+  if (env_int("STRATA_RING_EXCLUSIVE", kDefaultRingExclusive)) rp.smem_reserve = p->tma_smem;
+  if (p->gran < 16) rp.word_magic = div_magic(tok / p->gran, R * (tok / p->gran) + 32 * 4 * 32);
   for (int l = 0; l < p->d.num_layers; ++l) {
     rp.kb[l] = static_cast<char*>(p->k[l]);
     rp.vb[l] = static_cast<char*>(p->v[l]);
@@ -414,7 +438,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   // units, else the LDG engine (narrow rows R29, head-major tiers with several heads per GPU).  The
   // copy-engine path (STRATA_ENGINE_DMA) runs only when a caller asks for it.
   int engine = x->engine;
-  if (engine == STRATA_ENGINE_DEFAULT) engine = ring_supported(p) ? STRATA_ENGINE_TMA : STRATA_ENGINE_LDG;
+  if (engine == STRATA_ENGINE_DEFAULT) engine = ring_supported(p, dir) ? STRATA_ENGINE_TMA : STRATA_ENGINE_LDG;
   // the copy engines need long host runs: a token-major tier read in a head slice (Ht > H) has
   // only H*D*e bytes per token contiguous, so its DMA requests run on the LDG engine instead
   if (engine == STRATA_ENGINE_DMA && !dma_runs_ok(p)) engine = STRATA_ENGINE_LDG;
@@ -444,7 +468,13 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     return STRATA_OK;
   }
   RingParams rp;
-  if (engine == STRATA_ENGINE_TMA && !(ring_supported(p) && plan_ring(p, x, dir, xp, rp))) engine = STRATA_ENGINE_LDG;
+  int ctas = x->num_ctas;
+  if (engine == STRATA_ENGINE_TMA) {
+    const int c = ctas ? ctas : (dir == 0 ? kDefaultCtasRingLoad : kDefaultCtasRingOffload) *
+                                    (p->tok_bytes < kRingSmallRowBytes ? 2 : 1);
+    if (!(ring_supported(p, dir) && plan_ring(p, x, dir, xp, c, rp))) engine = STRATA_ENGINE_LDG;
+    else ctas = c;
+  }
   // the bulk rings stage whole host rows in 16-byte units: a head-major tier with > 1 head per GPU
   // has no whole rows, a pool whose rows / strides are not 16-byte multiples (R29) no 16-byte units
   if (engine == STRATA_ENGINE_TMA_BULK && (!p->host_row_contig() || p->gran < 16)) engine = STRATA_ENGINE_LDG;
@@ -465,10 +495,8 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   const int unroll = threads > 512 ? 4 : kDefaultUnroll;   // U=8 is compiled for <= 512 threads
   // lane t fetches row t; the warp then streams the 32 rows (amortised index math)
   xp.rows_per_group = 32;
-  int ctas = x->num_ctas;
   if (!ctas) {
-    if (engine == STRATA_ENGINE_TMA) ctas = dir == 0 ? kDefaultCtasRingLoad : kDefaultCtasRingOffload;
-    else if (engine == STRATA_ENGINE_TMA_BULK) ctas = kDefaultCtasTma;
+    if (engine == STRATA_ENGINE_TMA_BULK) ctas = kDefaultCtasTma;
     else if (p->gran < 16) ctas = kDefaultCtasNarrow;
     else ctas = dir == 0 ? kDefaultCtasLdg : kDefaultCtasLdgOffload;
     // small token rows shrink a bulk stage (<= 32 rows); keep ~64 KiB per stage-CTA in flight by
@@ -501,7 +529,12 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   if (engine == STRATA_ENGINE_TMA) {
     if (can_fuse) {
       if (!ring_batch(p, x, plan, plan.batches[0], rp)) return op_fail(cudaErrorInvalidValue, "ring piece count");
-      const int c = std::max(1, std::min(ctas, rp.npieces));
+      int c = std::max(1, std::min(ctas, rp.npieces));
+      // a small operation is latency-bound (one host round trip per piece in flight): spread its pieces
+      // over up to kSmallOpCtas CTAs so they are all in flight at once; it ends within microseconds,
+      // so the SM quota it briefly exceeds costs co-running work little
+      const int64_t op_bytes = int64_t(p->nkv) * plan.total_tokens * p->tok_bytes * (x->layer_end - x->layer_begin);
+      if (!x->num_ctas && op_bytes < kSmallOpBytes) c = std::max(c, std::min(kSmallOpCtas, rp.npieces));
       rp.l0 = x->layer_begin;
       rp.l1 = x->layer_end;
       rp.epoch = static_cast<uint32_t>(t);

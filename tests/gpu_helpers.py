@@ -11,15 +11,27 @@ import oracle
 from tests.helpers import CANARY
 
 
-def default_engine(g, strides=None) -> int:
-    """The engine strata_load/offload pick with STRATA_ENGINE_DEFAULT (transfer.cpp): the ring engine
-    (STRATA_ENGINE_TMA) when the tier has whole 16-byte host rows, else LDG (narrow rows R29, or a
-    head-major tier with several heads per GPU)."""
+def default_engine(g, strides=None, direction: str = "load") -> int:
+    """The engine strata_load/offload pick with STRATA_ENGINE_DEFAULT (transfer.cpp ring_supported):
+    the ring engine (STRATA_ENGINE_TMA) when the tier has whole host rows in 16-byte units — or, for
+    loads, narrow rows (R29) of 8- or 4-byte granularity whose host rows of a chunk form one run and
+    whose device rows are head-contiguous; else LDG (a head-major tier with several heads per GPU,
+    narrow offloads, 2- / 1-byte granularity).  Assumes a library-allocated (aligned) host tier."""
     import paper_2508_18572_b200 as st
-    vals = [g.H * g.D * g.e, g.D * g.e] + list(strides or ())
-    if any(v % 16 for v in vals) or (getattr(g, "head_major", False) and g.H > 1):
+    if getattr(g, "head_major", False) and g.H > 1:
         return st.STRATA_ENGINE_LDG
-    return st.STRATA_ENGINE_TMA
+    vals = [g.H * g.D * g.e, g.D * g.e] + list(strides or ())
+    gran = 16
+    for v in vals:
+        while gran > 1 and v % gran:
+            gran //= 2
+    if gran == 16:
+        return st.STRATA_ENGINE_TMA
+    Ht = getattr(g, "Ht", 0) or g.H
+    head_contig = strides is None or strides[2] == g.D * g.e or g.H == 1
+    if direction == "load" and gran in (8, 4) and Ht == g.H and head_contig:
+        return st.STRATA_ENGINE_TMA
+    return st.STRATA_ENGINE_LDG
 
 
 def nhd(g):

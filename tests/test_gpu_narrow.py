@@ -48,7 +48,7 @@ def test_narrow_rows(engine, kv, H, D, e):
     _run(g, q, engine, seed=D)
 
 
-@pytest.mark.parametrize("engine", [st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_DMA])
+@pytest.mark.parametrize("engine", [st.STRATA_ENGINE_LDG, st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_DMA])
 @pytest.mark.parametrize("layout", ["hnd", "padded", "head_major_slice"])
 def test_narrow_layouts(engine, layout):
     H, D, e, P = 3, 10, 2, 4
@@ -65,15 +65,16 @@ def test_narrow_layouts(engine, layout):
 
 @pytest.mark.parametrize("C", [64, 256])
 def test_narrow_layer_sized_default_engine(C):
-    """>= 4 MiB per layer of 72-byte fp8 rows: the default engine is the narrow zero-copy LDG kernel
-    in both directions (the copy engines run only when a caller asks for STRATA_ENGINE_DMA)."""
+    """>= 4 MiB per layer of 72-byte fp8 rows: the default engine is zero-copy in both directions —
+    the ring engine's narrow-word path for loads, the narrow LDG kernel for offloads (the copy
+    engines run only when a caller asks for STRATA_ENGINE_DMA)."""
     g = Geometry(L=2, H=1, D=72, e=1, P=1, C=C, num_pages=40000, num_chunks=38400 // C)
     q = kvgen.make_requests(kvgen.rng_for(121), [32000], g.P, g.C, g.num_pages, g.num_chunks)
     c = GpuCase(g, q, seed=4)
     try:
         c.pool.load(c.reqs)
         torch.cuda.synchronize()
-        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_LDG
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_TMA
         c.check_load(0, g.L)
         before = c.pool.host.copy()
         for t in c.k + c.v:

@@ -154,6 +154,34 @@ def test_special_float_payloads(engine):
         c.close()
 
 
+@pytest.mark.parametrize("engine", [st.STRATA_ENGINE_DEFAULT, st.STRATA_ENGINE_TMA, st.STRATA_ENGINE_LDG])
+@pytest.mark.parametrize("H,D,e,P", [(3, 16, 2, 1), (5, 16, 2, 4), (1, 40, 2, 1), (3, 64, 2, 16), (7, 16, 2, 1),
+                                     (1, 24, 2, 2), (9, 16, 2, 1), (3, 32, 1, 8)])
+@pytest.mark.parametrize("strides", ["nhd", "hnd"])
+def test_rows_with_odd_vector_counts(engine, H, D, e, P, strides):
+    """Rows of 3, 5, 6, 7, 9, 10 ... 16-byte vectors (not a power of two, fewer than 32): the ring
+    engine moves 32 / vpt rows per warp instruction, and with 64-row pieces a group straddles row 32
+    (two address slots per lane).  Partial chunks and pages, several requests, both directions."""
+    g = Geometry(3, H, D, e, P, 64, -(-1400 // P) + 8, 40)
+    tok = g.token_bytes
+    st_ = (g.H * P * g.D * g.e, g.D * g.e, P * g.D * g.e) if strides == "hnd" else None
+    q = kvgen.make_requests(kvgen.rng_for(13 + H + D), [700, 129, 64, 1], g.P, g.C, g.num_pages, g.num_chunks,
+                            offsets=True)
+    c = GpuCase(g, q, strides=st_, seed=H * D)
+    try:
+        c.pool.load(c.reqs, engine=engine)
+        _sync()
+        c.check_load(0, g.L)
+        before = c.pool.host.copy()
+        for t in c.k + c.v:
+            t.copy_(torch.randint(0, 256, t.shape, dtype=torch.uint8, device="cuda"))
+        c.pool.offload(c.reqs, 1, 3, engine=engine)
+        _sync()
+        assert np.array_equal(c.pool.host, c.expected_offload(before, 1, 3)), (tok, engine)
+    finally:
+        c.close()
+
+
 @pytest.mark.parametrize("direction", ["load", "offload"])
 @pytest.mark.parametrize("group", [1, 2, 4])
 def test_dma_engine_multi_piece(direction, group):

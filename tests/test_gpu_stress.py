@@ -36,6 +36,8 @@ def _case(i):
     head_major = bool(rng.integers(0, 2)) and Ht > 1
     # 16-byte rows mostly; a fifth of the cases take narrow rows (R29: 3..72-byte heads)
     D = int(rng.choice([3, 10, 36, 72])) if rng.random() < 0.2 else int(rng.choice([64, 128, 576] if H == 1 else [64, 128]))
+    if rng.random() < 0.15:   # rows of a non-power-of-two count of 16-byte vectors (ring: groups straddling row 32)
+        D = int(rng.choice([24, 40, 48, 88, 200]))
     e = int(rng.choice([1, 2]))
     P = int(rng.choice([1, 2, 8, 16, 64]))
     C = int(rng.choice([1, 8, 64, 128]))

@@ -107,21 +107,27 @@ def main():
                     help="ring engine (engine 2) shared-memory budgets per CTA in KiB (0 = all): bounds the host "
                          "bytes in flight (STRATA_RING_SMEM_KB)")
     ap.add_argument("--ring-stage", default="0", help="ring engine piece sizes in KiB (0 = default; STRATA_RING_STAGE_KB)")
+    ap.add_argument("--ring-configs", default="",
+                    help="explicit ring geometries 'ctas:stage_kb:smem_kb:warps,...' (replaces the engine x ctas grid)")
     ap.add_argument("--memcpy", type=int, default=0, help="also co-run a contiguous cudaMemcpyAsync loop (-1 engine)")
     ap.add_argument("--cooldown", type=float, default=1.0,
                     help="idle seconds before every alone / co-run block (power-state reset for the GEMM proxy)")
     ap.add_argument("--graph", type=int, default=0,
                     help="replay each proxy from a CUDA graph (as serving engines run decode): copy-engine "
                          "traffic delays the per-kernel launch fetches of eager proxies (ce_interference.py)")
+    ap.add_argument("--layers", type=int, default=0, help="override L of the Llama-8B load (device-pool footprint)")
+    ap.add_argument("--P", type=int, default=1, help="device page size")
+    ap.add_argument("--flags", type=int, default=0, help="strata_pool_desc.flags of the host tier (1 = huge pages)")
+    ap.add_argument("--tag", default="")
     args = ap.parse_args()
 
-    g = kvgen.geometry("llama8b_32k")
+    g = kvgen.geometry("llama8b_32k", P=args.P, **({"L": args.layers} if args.layers else {}))
     q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks)
     nb = g.num_pages * g.P * g.token_bytes
     k = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
     v = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
     pool = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=g.P, chunk_tokens=g.C,
-                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks)
+                       k_ptrs=k, v_ptrs=v, num_pages=g.num_pages, num_chunks=g.num_chunks, flags=args.flags)
     reqs = st.Requests.from_kvgen(q)
     bytes_load = 2 * g.L * q.total_tokens * g.token_bytes
     lo, hi = torch.cuda.Stream.priority_range()
@@ -145,7 +151,8 @@ def main():
     scratch = torch.empty(bytes_load // g.L, dtype=torch.uint8, device="cuda")
 
     def make_io(eng, c, G, env):
-        for key in ("STRATA_RING_SMEM_KB", "STRATA_RING_STAGE_KB"):
+        for key in ("STRATA_RING_SMEM_KB", "STRATA_RING_STAGE_KB", "STRATA_RING_WARPS", "STRATA_RING_DEBUG",
+                    "STRATA_RING_EXCLUSIVE"):
             os.environ.pop(key, None)
         os.environ.update(env)
         if eng < 0:   # contiguous memcpy of the same bytes: 32 copies of one layer's worth
@@ -166,6 +173,17 @@ def main():
                             for m in args.ring_smem.split(",") for k_ in args.ring_stage.split(",")]
                 for env in envs:
                     configs.append((eng, c, G, env))
+    if args.ring_configs:
+        configs = []
+        for spec in args.ring_configs.split(","):
+            f = spec.split(":")
+            c, skb, smem, w = (int(x) for x in f[:4])
+            env = {"STRATA_RING_STAGE_KB": str(skb), "STRATA_RING_SMEM_KB": str(smem), "STRATA_RING_WARPS": str(w)}
+            if len(f) > 4:   # optional 5th field: STRATA_RING_EXCLUSIVE (reserve the SM's shared memory)
+                env["STRATA_RING_EXCLUSIVE"] = f[4]
+            if len(f) > 5:   # optional 6th field: STRATA_RING_DEBUG bits (A/B only)
+                env["STRATA_RING_DEBUG"] = f[5]
+            configs.append((2, c, 0, env))
     if args.memcpy:
         configs.append((-1, 0, 0, {}))
     for eng, c, G, env in configs:
@@ -205,8 +223,8 @@ def main():
                     b.synchronize()
                     io_cos.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
                 al, co = statistics.median(alone_ms), statistics.median(co_ms)
-                print(json.dumps({"kind": "corun", "graph": args.graph, "engine": eng, "ctas": c, "layer_group": G,
-                                  "env": env,
+                print(json.dumps({"kind": "corun", "tag": args.tag, "L": g.L, "P": g.P, "flags": args.flags,
+                                  "graph": args.graph, "engine": eng, "ctas": c, "layer_group": G, "env": env,
                                   "proxy": name, "proxy_alone_ms": round(al, 4), "proxy_corun_ms": round(co, 4),
                                   "slowdown": round(co / al - 1, 4),
                                   "slowdown_rounds": [round(x / y - 1, 4) for x, y in zip(co_ms, alone_ms)],

@@ -48,12 +48,13 @@ def main():
     ap.add_argument("--frag", default="perm", help="page table: perm | identity | churn")
     ap.add_argument("--chunk-frag", default="perm", help="host chunk order: perm | identity")
     ap.add_argument("--tag", default="")
+    ap.add_argument("--layers", type=int, default=0, help="override L (0 = the config's)")
     ap.add_argument("--bulk-store", default="0", help="load: 0 st.global scatter, 1 cp.async.bulk stores (list)")
     args = ap.parse_args()
     io = torch.cuda.Stream()
     for spec in args.configs.split(","):
         name, P = spec.split(":")
-        g = kvgen.geometry(name, P=int(P))
+        g = kvgen.geometry(name, P=int(P), **({"L": args.layers} if args.layers else {}))
         q = kvgen.make_requests(kvgen.rng_for(1), kvgen.CONFIGS[name]["n"], g.P, g.C, g.num_pages, g.num_chunks,
                                 frag=args.frag, chunk_frag=args.chunk_frag)
         nb = g.num_pages * g.P * g.token_bytes
@@ -101,7 +102,7 @@ def main():
                                      for l in check_layers)
                         else:
                             ok = bool((pool.host == host_ref).all())   # loaded from this tier: offload rewrites the same bytes
-                        print(json.dumps({"kind": "ring", "tag": args.tag, "flags": args.flags, "frag": args.frag,
+                        print(json.dumps({"kind": "ring", "tag": args.tag, "L": g.L, "flags": args.flags, "frag": args.frag,
                                           "chunk_frag": args.chunk_frag, "config": name, "P": g.P, "dir": d, "ctas": c, "warps": w,
                                           "stage_kb": skb, "bulk_store": int(bs), "gbs": round(r, 2),
                                           "frac_link": round(r / (link if d == "load" else link_d2h), 4),
