@@ -42,7 +42,7 @@ PATH_DESC = {
             "(one cp.async.bulk per page-first host run of <= 32 KiB, from the UVA-mapped tier) + 8 LSU scatter "
             "warps (16-byte st.global to the pages); per-layer completion flags -> layer events",
     "ldg": "ldg_fused_kernel (csrc/kernels.cu): zero-copy 16-byte LDG/STG register staging, one launch for all layers",
-    "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (cudaMemcpyBatchAsync) into an HBM "
+    "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (one cudaMemcpyAsync per run) into an HBM "
            "staging slot + ldg_kernel scatter to the pages",
     "tma_bulk": "tma_kernel (csrc/kernels.cu): one warp per CTA, cp.async.bulk on both sides of a smem ring",
 }

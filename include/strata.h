@@ -61,7 +61,6 @@
  *   STRATA_DMA_EDGE_SPLIT=n    first / last layer in n times smaller pieces (default 4; 1 = off)
  *   STRATA_DMA_ORDERED=0       drop the per-piece barrier between copy streams (default on)
  *   STRATA_DMA_STRIDED=0       one copy per chunk instead of strided runs of consecutive chunks
- *   STRATA_DMA_NO_BATCH=1      plain cudaMemcpyAsync instead of cudaMemcpyBatchAsync
  *
  * THREADING: a pool handle is single-writer (one thread at a time); distinct handles are
  * independent.  Operations of one handle may be in flight at once on different streams (e.g. a
@@ -127,8 +126,8 @@ enum strata_engine {
                                  cp.async.bulk through a shared-memory ring, LSU warps scatter the
                                  rows to their pages (offload: cp.async gather, bulk host store) */
   STRATA_ENGINE_TMA_BULK = 3, /* one warp per CTA, cp.async.bulk on both sides of the ring */
-  STRATA_ENGINE_DMA = 4       /* copy-engine gather of whole page-first host runs (cudaMemcpyBatchAsync,
-                                 one in-order copy stream) into a double-buffered HBM staging ring + the LDG
+  STRATA_ENGINE_DMA = 4       /* copy-engine gather of whole page-first host runs (one cudaMemcpyAsync
+                                 per run, one in-order copy stream) into a double-buffered HBM staging ring + the LDG
                                  kernel scattering staged rows to their pages (offload: the mirror).
                                  Needs strata_xfer.host_chunks_host. */
 };

@@ -28,12 +28,6 @@ enum strata_dir { STRATA_H2D = 0, STRATA_D2H = 1 };
 int strata_baseline_memcpy_pages(strata_pool_t p, const strata_xfer* x, int32_t dir,
                                  strata_stream_t stream, int64_t* ncopies);
 
-/* The same copy list submitted through cudaMemcpyBatchAsync (CUDA >= 12.8), the modern DMA
- * baseline, in batches of at most 65536 copies.  Returns STRATA_ERR_UNSUPPORTED if the runtime
- * lacks it. */
-int strata_baseline_memcpy_batch(strata_pool_t p, const strata_xfer* x, int32_t dir,
-                                 strata_stream_t stream, int64_t* ncopies);
-
 /* The link roofline: ONE contiguous cudaMemcpyAsync of `bytes` between the registered host tier
  * (starting `host_offset` bytes in) and device memory `dev` (the denominator). */
 int strata_baseline_contiguous(strata_pool_t p, int32_t dir, void* dev, int64_t host_offset,

@@ -7,7 +7,7 @@ by callers for device memory and streams only.
     strata_register_host_pool / strata_unregister_host_pool / strata_host_pool_ptr
     strata_load / strata_offload            -> ticket
     strata_layer_event / strata_wait_layer / strata_layer_elapsed_ms
-    strata_baseline_memcpy_pages / strata_baseline_memcpy_batch / strata_baseline_contiguous
+    strata_baseline_memcpy_pages / strata_baseline_contiguous
 
 Plus two conveniences: :class:`HostPool` (owns a registered pool, exposes the host tier as a numpy
 array) and :class:`Requests` (request tables with device-resident index lists).
@@ -29,7 +29,7 @@ from ._lib import (STRATA_D2H, STRATA_ENGINE_DEFAULT, STRATA_ENGINE_LDG, STRATA_
 __all__ = [
     "strata_register_host_pool", "strata_unregister_host_pool", "strata_host_pool_ptr", "strata_load",
     "strata_offload", "strata_layer_event", "strata_wait_layer", "strata_layer_elapsed_ms",
-    "strata_baseline_memcpy_pages", "strata_baseline_memcpy_batch", "strata_baseline_contiguous",
+    "strata_baseline_memcpy_pages", "strata_baseline_contiguous",
     "strata_version", "strata_get_counters", "HostPool", "Requests", "StrataError",
 ]
 
@@ -111,14 +111,6 @@ def strata_baseline_memcpy_pages(pool: int, xfer: Xfer, direction: int, stream=N
     check(_lib.lib().strata_baseline_memcpy_pages(ctypes.c_void_p(pool), ctypes.byref(xfer), direction,
                                                   ctypes.c_void_p(_stream_handle(stream)), ctypes.byref(n)),
           "strata_baseline_memcpy_pages")
-    return int(n.value)
-
-
-def strata_baseline_memcpy_batch(pool: int, xfer: Xfer, direction: int, stream=None) -> int:
-    n = ctypes.c_int64()
-    check(_lib.lib().strata_baseline_memcpy_batch(ctypes.c_void_p(pool), ctypes.byref(xfer), direction,
-                                                  ctypes.c_void_p(_stream_handle(stream)), ctypes.byref(n)),
-          "strata_baseline_memcpy_batch")
     return int(n.value)
 
 

@@ -109,8 +109,6 @@ _SIGS = {
     "strata_version": (ctypes.c_int, []),
     "strata_baseline_memcpy_pages": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Xfer), ctypes.c_int32,
                                                     ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
-    "strata_baseline_memcpy_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Xfer), ctypes.c_int32,
-                                                    ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "strata_baseline_contiguous": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                                   ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
 }

@@ -4,7 +4,6 @@
 // registered host tier, so the comparison isolates the transfer mechanism:
 //   * per-page cudaMemcpyAsync loop — the paper's fragmentation baseline (PAPER.md:166-169, :182
 //     ~22 % of PCIe 5.0 at P=32; SGLang-HiCache),
-//   * the same copy list through cudaMemcpyBatchAsync (CUDA 12.8+),
 //   * one contiguous cudaMemcpyAsync (the measured link roofline).
 #include <cuda_runtime.h>
 
@@ -109,40 +108,6 @@ int strata_baseline_memcpy_pages(strata_pool_t p, const strata_xfer* x, int32_t 
   if (rc) return rc;
   if (err != cudaSuccess) return bfail(STRATA_ERR_CUDA, "cudaMemcpyAsync", err);
   if (ncopies) *ncopies = count;
-  return STRATA_OK;
-}
-
-int strata_baseline_memcpy_batch(strata_pool_t p, const strata_xfer* x, int32_t dir, strata_stream_t stream,
-                                 int64_t* ncopies) {
-  if (dir != STRATA_H2D && dir != STRATA_D2H) return bfail(STRATA_ERR_INVALID_ARG, "bad dir");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  std::vector<void*> dsts, srcs;
-  std::vector<size_t> sizes;
-  int rc = for_each_copy(p, x, dir, [&](const Copy& c) {
-    dsts.push_back(c.dst);
-    srcs.push_back(const_cast<void*>(c.src));
-    sizes.push_back(c.bytes);
-  });
-  if (rc) return rc;
-  cudaMemcpyAttributes attr;
-  memset(&attr, 0, sizeof attr);
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = dir == STRATA_H2D ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
-  attr.srcLocHint.id = dir == STRATA_H2D ? 0 : p->d.device;
-  attr.dstLocHint.type = dir == STRATA_H2D ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
-  attr.dstLocHint.id = dir == STRATA_H2D ? p->d.device : 0;
-  size_t attr_idx = 0;
-  const size_t kBatch = 16384;
-  for (size_t lo = 0; lo < dsts.size(); lo += kBatch) {
-    const size_t cnt = std::min(kBatch, dsts.size() - lo);
-    size_t fail_idx = 0;
-    cudaError_t e = cudaMemcpyBatchAsync(dsts.data() + lo, srcs.data() + lo, sizes.data() + lo, cnt, &attr,
-                                         &attr_idx, 1, &fail_idx, s);
-    if (e == cudaErrorNotSupported || e == cudaErrorCallRequiresNewerDriver)
-      return bfail(STRATA_ERR_UNSUPPORTED, "cudaMemcpyBatchAsync", e);
-    if (e != cudaSuccess) return bfail(STRATA_ERR_CUDA, "cudaMemcpyBatchAsync", e);
-  }
-  if (ncopies) *ncopies = static_cast<int64_t>(dsts.size());
   return STRATA_OK;
 }
 

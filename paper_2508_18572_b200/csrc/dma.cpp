@@ -17,8 +17,9 @@ namespace strata {
 // The page-first host tier keeps, for one layer, the K rows and then the V rows of a chunk's C
 // tokens back to back (R1), so a layer of a fully covered chunk is ONE contiguous 2*C*S_tok run
 // (256 KiB for Llama-8B at C=64).  The copy engines read such runs at up to 98 % of the link
-// (cudaMemcpyBatchAsync of 256 KiB copies over 4 streams, profiles/r01/ce_probe.jsonl) where
-// SM-issued reads top out at 92.6 %.  Each run lands in an HBM staging slot laid out exactly like
+// (256 KiB copies, profiles/r01/ce_probe.jsonl) where SM-issued reads top out at 92.6 %.  Each run
+// is one cudaMemcpyAsync (the batched submission API of round 1 is closed on the GPU pool after
+// unexplained Xid 32 faults).  Each run lands in an HBM staging slot laid out exactly like
 // a compact host tier with one layer (slot j = [K rows][V rows] of C tokens), so the unchanged LDG
 // kernel scatters it to the pages with chunk index = slot index.  Two slots alternate so the copy
 // engines fill one while the SMs scatter the other.
@@ -124,45 +125,22 @@ struct Copy2D {
   size_t spitch, width, height;
 };
 
-// Submit a copy list over the pool's copy streams (contiguous shares, one batch call each); the
-// strided runs go to the first stream.
+// Submit a copy list over the pool's copy streams (contiguous shares, one cudaMemcpyAsync per run);
+// the strided runs go to the first stream.
 static cudaError_t submit_copies(strata_pool* p, strata_pool::DmaDir& D, std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sz,
                           const std::vector<Copy2D>& c2d, int dir, int slot) {
-  cudaMemcpyAttributes attr;
-  memset(&attr, 0, sizeof attr);
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.srcLocHint.type = dir == 0 ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
-  attr.srcLocHint.id = dir == 0 ? 0 : p->d.device;
-  attr.dstLocHint.type = dir == 0 ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
-  attr.dstLocHint.id = dir == 0 ? p->d.device : 0;
+  (void)p;
   const size_t n = dst.size();
   const int ns = D.ncs;
-  // cudaMemcpyBatchAsync refuses stream capture; under capture the copies become plain memcpy nodes
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaError_t e0 = cudaStreamIsCapturing(D.cs[0], &cap);
-  if (e0 != cudaSuccess) return e0;
   const cudaMemcpyKind kind = dir == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
   for (const Copy2D& r : c2d) {
     cudaError_t e = cudaMemcpy2DAsync(r.dst, r.dpitch, r.src, r.spitch, r.width, r.height, kind, D.cs[0]);
     if (e != cudaSuccess) return e;
   }
-  // env STRATA_DMA_NO_BATCH=1: plain cudaMemcpyAsync per run (A/B and tools that do not model the
-  // batch API, e.g. compute-sanitizer initcheck)
-  static const bool no_batch = [] {
-    const char* v = getenv("STRATA_DMA_NO_BATCH");
-    return v && atoi(v) != 0;
-  }();
   for (int c = 0; c < ns; ++c) {
     const size_t lo = n * c / ns, hi = n * (c + 1) / ns;
-    if (hi > lo && (cap == cudaStreamCaptureStatusActive || no_batch)) {
-      for (size_t i = lo; i < hi; ++i) {
-        cudaError_t e = cudaMemcpyAsync(dst[i], src[i], sz[i], kind, D.cs[c]);
-        if (e != cudaSuccess) return e;
-      }
-    } else if (hi > lo) {
-      size_t idx = 0, fail_idx = 0;
-      cudaError_t e = cudaMemcpyBatchAsync(dst.data() + lo, src.data() + lo, sz.data() + lo, hi - lo, &attr, &idx, 1,
-                                           &fail_idx, D.cs[c]);
+    for (size_t i = lo; i < hi; ++i) {
+      cudaError_t e = cudaMemcpyAsync(dst[i], src[i], sz[i], kind, D.cs[c]);
       if (e != cudaSuccess) return e;
     }
     cudaError_t e = cudaEventRecord(D.ev_copy[slot][c], D.cs[c]);
@@ -445,7 +423,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
             for (int cj = 0; cj < ncs; ++cj)
               if (cj != ci && (e = cudaStreamWaitEvent(D.cs[ci], D.ev_copy[slot ^ 1][cj], 0)))
                 return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, D, cl.dst, cl.src, cl.sz, cl.c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        if ((e = submit_copies(p, D, cl.dst, cl.src, cl.sz, cl.c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyAsync (DMA runs)");
         for (int ci = 0; ci < ncs; ++ci)
           if ((e = cudaStreamWaitEvent(s, D.ev_copy[slot][ci], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
         if ((e = launch_group(0))) return cuda_fail(e, "scatter kernel launch");
@@ -459,7 +437,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
         if ((e = cudaEventRecord(D.ev_slot[slot], s))) return cuda_fail(e, "cudaEventRecord");
         for (int ci = 0; ci < ncs; ++ci)
           if ((e = cudaStreamWaitEvent(D.cs[ci], D.ev_slot[slot], 0))) return cuda_fail(e, "cudaStreamWaitEvent");
-        if ((e = submit_copies(p, D, cl.dst, cl.src, cl.sz, cl.c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyBatchAsync");
+        if ((e = submit_copies(p, D, cl.dst, cl.src, cl.sz, cl.c2d, dir, slot))) return cuda_fail(e, "cudaMemcpyAsync (DMA runs)");
       }
       p->counters.dma_copies += static_cast<int64_t>(cl.dst.size());
       last_slot = slot;

@@ -294,7 +294,7 @@ def test_baselines_match_oracle(variant):
          "narrow": Geometry(3, 3, 10, 2, 4, 16, 96, 24)}[variant]
     rng = kvgen.rng_for(8)
     q = kvgen.make_requests(rng, [37, 100, 5], g.P, g.C, g.num_pages, g.num_chunks, offsets=True)
-    for fn in (st.strata_baseline_memcpy_pages, st.strata_baseline_memcpy_batch):
+    for fn in (st.strata_baseline_memcpy_pages,):
         c = GpuCase(g, q)
         try:
             s = torch.cuda.Stream()

@@ -1,6 +1,7 @@
 // Copy-engine probe: how fast can DMA move chunk-sized host runs (SURVEY.md §8f hybrid variant)?
 // H2D copies of S bytes each from random positions of a pinned host buffer into a contiguous device
-// staging buffer, submitted as a cudaMemcpyAsync loop or cudaMemcpyBatchAsync, over 1..4 streams.
+// staging buffer, submitted as a cudaMemcpyAsync loop, over 1..4 streams (round 1 also timed a batched
+// submission; that API is closed on the GPU pool after Xid 32 faults).
 // One JSON object per line.
 //
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ce_probe ce_probe.cu
@@ -44,7 +45,7 @@ int main() {
       dsts[i] = d + i * S;
       srcs[i] = h + slot[i] * S;
     }
-    for (int mode = 0; mode < 2; ++mode) {
+    for (int mode = 0; mode < 1; ++mode) {
       for (int nstreams : {1, 2, 4}) {
         std::vector<float> ms;
         std::vector<double> wall;
@@ -57,20 +58,7 @@ int main() {
           for (int k = 0; k < nstreams; ++k) {
             const size_t lo = k * per, hi = std::min(n, lo + per);
             if (lo >= hi) continue;
-            if (mode == 0) {
-              for (size_t i = lo; i < hi; ++i) CK(cudaMemcpyAsync(dsts[i], srcs[i], S, cudaMemcpyHostToDevice, ss[k]));
-            } else {
-              cudaMemcpyAttributes attr;
-              memset(&attr, 0, sizeof attr);
-              attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-              attr.srcLocHint.type = cudaMemLocationTypeHost;
-              attr.dstLocHint.type = cudaMemLocationTypeDevice;
-              size_t idx = 0, fail = 0;
-              for (size_t b = lo; b < hi; b += 4096) {
-                const size_t c = std::min<size_t>(4096, hi - b);
-                CK(cudaMemcpyBatchAsync(dsts.data() + b, srcs.data() + b, sizes.data() + b, c, &attr, &idx, 1, &fail, ss[k]));
-              }
-            }
+            for (size_t i = lo; i < hi; ++i) CK(cudaMemcpyAsync(dsts[i], srcs[i], S, cudaMemcpyHostToDevice, ss[k]));
             if (k) {
               CK(cudaEventRecord(done[k], ss[k]));
               CK(cudaStreamWaitEvent(ss[0], done[k]));
@@ -90,7 +78,7 @@ int main() {
         std::sort(wall.begin(), wall.end());
         const float m = ms[ms.size() / 2];
         printf("{\"kind\":\"ce\",\"mode\":\"%s\",\"copy_bytes\":%zu,\"copies\":%zu,\"streams\":%d,\"ms\":%.3f,"
-               "\"wall_ms\":%.3f,\"gbs\":%.2f}\n", mode ? "batch" : "loop", S, n, nstreams, m, wall[wall.size() / 2],
+               "\"wall_ms\":%.3f,\"gbs\":%.2f}\n", "loop", S, n, nstreams, m, wall[wall.size() / 2],
                total / m / 1e6);
         fflush(stdout);
       }

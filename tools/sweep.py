@@ -2,7 +2,7 @@
 """Sweep the load/offload kernels and the copy-engine baselines on one GPU.
 
 For each page size: engine x SM quota (num_ctas) for strata_load and strata_offload, the per-page
-cudaMemcpyAsync loop, cudaMemcpyBatchAsync, and the contiguous memcpy roofline, all from the same
+cudaMemcpyAsync loop and the contiguous memcpy roofline, all from the same
 registered host tier.  One JSON object per line on stdout.
 
     python tools/sweep.py [--config llama8b_32k] [--pages 1,16] [--ctas 1,2,4,8,16,32,148]
@@ -90,8 +90,7 @@ def main():
                                       "ms": round(ev * 1e3, 3), "wall_ms": round(wall * 1e3, 3),
                                       "gbs": round(nbytes / ev / 1e9, 3)}), flush=True)
         if args.baselines == "1":
-            for name, fn in (("memcpy_pages", st.strata_baseline_memcpy_pages),
-                             ("memcpy_batch", st.strata_baseline_memcpy_batch)):
+            for name, fn in (("memcpy_pages", st.strata_baseline_memcpy_pages),):
                 for d, dd in (("h2d", st.STRATA_H2D), ("d2h", st.STRATA_D2H)):
                     x = reqs.xfer(0, g.L, host_lists=True)
                     cnt = [0]
