@@ -346,13 +346,18 @@ def main(argv=None):
             dist.barrier()
         torch.cuda.synchronize()
 
+    submit_s = [0.0]
+
     def timed(fn, n):
-        """n back-to-back calls on `io`: (seconds, per-call ms) from CUDA events on the I/O stream."""
+        """n back-to-back calls on `io`: (seconds, per-call ms) from CUDA events on the I/O stream;
+        submit_s[0] = host seconds spent issuing them (before the final synchronize)."""
         marks = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
+        h = time.perf_counter()
         marks[0].record(io)
         for i in range(n):
             fn()
             marks[i + 1].record(io)
+        submit_s[0] = time.perf_counter() - h
         marks[-1].synchronize()
         per = [marks[i].elapsed_time(marks[i + 1]) for i in range(n)]
         return marks[0].elapsed_time(marks[-1]) / 1e3, per
@@ -378,9 +383,8 @@ def main(argv=None):
         barrier()
         c0 = pool.counters()
         with ClockSampler(local) as clocks:
-            h0 = time.perf_counter()
             elapsed, step_ms = timed(step, args.steps)
-            host_s = time.perf_counter() - h0
+            host_s = submit_s[0]
             last = pool.counters()
             barrier()
         return elapsed, sorted(step_ms), host_s, clocks, last["kernel_launches"] - c0["kernel_launches"], last
@@ -478,6 +482,22 @@ def main(argv=None):
             ee, _ = timed(fe, 3)
             others[ENGINE_NAMES[eng]] = round(bytes_step * 3 / ee / 1e9, 3)
         extras["other_engines_gbs"] = others
+        if bytes_step < (16 << 20):
+            # a small load is bound by host submission (the Python call + the library's launch work,
+            # ~20 us) more than by the device: the same load captured once into a CUDA graph and
+            # replayed (per-layer launches inside the graph; tests/test_gpu_graph.py)
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, stream=io):
+                step()
+
+            def replay():
+                with torch.cuda.stream(io):
+                    cg.replay()
+            replay()
+            eg, per_g = timed(replay, max(10, args.steps))
+            extras["graph_replay"] = {"ms_per_step": round(statistics.median(per_g), 4),
+                                      "value": round(bytes_step / (statistics.median(per_g) / 1e3) / 1e9, 3),
+                                      "steps": max(10, args.steps)}
     del scratch
 
     out = None

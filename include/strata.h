@@ -191,7 +191,9 @@ typedef struct {
  * element size; the library page-locks and maps it (cudaHostRegisterMapped|Portable) and
  * unregisters it when the LAST pool whose tier lies inside that registration closes (several pools
  * — e.g. the TP ranks of one process — may share one caller tier); memory the caller registered
- * itself is never unregistered by the library; the caller keeps ownership.  If NULL, the library allocates it
+ * itself is never unregistered by the library; the caller keeps ownership.  A range that overlaps an
+ * open pool's caller tier without lying inside it is rejected (INVALID_ARG): register the enclosing
+ * range first.  If NULL, the library allocates it
  * (NUMA-local to the GPU, pre-touched, optionally huge pages / write-combined), owns and frees it.
  * Device buffers stay caller-owned and must outlive the handle.
  * Errors: INVALID_ARG, ALIGNMENT, OOM, CUDA.  On error *out is set to NULL. */

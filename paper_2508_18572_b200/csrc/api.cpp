@@ -176,6 +176,10 @@ cudaError_t register_caller(char* base, size_t bytes, bool& ours) {
       ours = true;
       return cudaSuccess;
     }
+  // a range that overlaps one of the library's registrations without lying inside it cannot share
+  // it (the registration would be undone under this pool when the other pools close)
+  for (const auto& r : g_regs)
+    if (base < r.base + r.bytes && r.base < base + bytes) return cudaErrorHostMemoryAlreadyRegistered;
   cudaError_t e = cudaHostRegister(base, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
   if (e == cudaErrorHostMemoryAlreadyRegistered) {
     cudaGetLastError();
@@ -298,6 +302,12 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
     p->host_kind = 0;
     bool ours = false;
     e = register_caller(p->host, p->host_bytes, ours);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      p->host = nullptr;
+      delete p;
+      return fail(STRATA_ERR_INVALID_ARG, "host_base range overlaps the host tier of another open pool without "
+                  "lying inside it (pools may share a tier only when one range contains the other's)");
+    }
     if (e != cudaSuccess) {
       p->host = nullptr;
       delete p;

@@ -279,6 +279,12 @@ constexpr int kDefaultRingWarps = 8;         // load: scatter warps
 constexpr int kDefaultRingGatherWarps = 8;   // offload: cp.async gather warps
 constexpr int kDefaultRingStageKB = 16;
 constexpr int kDefaultRingInflightKB = 224;  // host bytes in flight over all CTAs (2 CTAs: 7 x 16 KiB each)
+// Rows shorter than 2 KiB keep their stages longer on the device side (more rows, more page-table
+// entries, and for 1152-byte MLA rows a non-power-of-two vector count per piece), so fewer of the
+// ring's bytes are on the link at any moment: 224 KiB moves 44.7 GB/s for 256-byte rows (70B TP=8, 4
+// CTAs) and 45.7 for 1152-byte rows (2 CTAs), 320 KiB 50.4 / 51.0 (profiles/r02/sweep70/).
+constexpr int kRingShortRowBytes = 2048;
+constexpr int kDefaultRingInflightShortKB = 320;
 constexpr int kDefaultRingExclusive = 0;     // 1: a ring CTA reserves its SM's shared memory
 constexpr int kTmaStageTarget = 32 << 10;
 

@@ -313,17 +313,28 @@ static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const
   // (strata_xfer.inflight_kib), else the default — the knee of the throughput / interference
   // frontier: more than the link needs only queues requests, and queued host reads
   // are what slows co-running HBM-bound work
-  const int64_t total = x->inflight_kib > 0 ? x->inflight_kib : env_int("STRATA_RING_INFLIGHT_KB", kDefaultRingInflightKB);
+  const int64_t total = x->inflight_kib > 0 ? x->inflight_kib
+                        : env_int("STRATA_RING_INFLIGHT_KB", tok < kRingShortRowBytes ? kDefaultRingInflightShortKB
+                                                                                     : kDefaultRingInflightKB);
   const int64_t per_cta = (total << 10) / std::max(1, ctas);
   int S = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(kRingMaxStages, per_cta / sb)));
   S = std::min(S, env_int("STRATA_RING_STAGES", kRingMaxStages));
   while (S >= 2 && ring_header_bytes() + S * sb > budget) --S;
   if (S < 2) return false;
-  // stage s belongs to device-side warp s % W (ring.cu), so W must divide S: the ring capacity S
-  // (the host bytes in flight) is kept and W becomes the largest divisor of S not above the request
+  // stage s belongs to device-side warp s % W (ring.cu), so W must divide S: take the largest S' <= S
+  // with a divisor d <= W of at least half of min(W, S') and run d warps (S = 13, W = 8 would otherwise
+  // leave ONE scatter warp: 16.4 GB/s instead of 51, profiles/r02/sweep70/)
   int Wd = 1;
-  for (int d = 1; d <= std::min(W, S); ++d)
-    if (S % d == 0) Wd = d;
+  for (int s2 = S; s2 >= 2; --s2) {
+    int d = 1;
+    for (int c = 1; c <= std::min(W, s2); ++c)
+      if (s2 % c == 0) d = c;
+    if (2 * d >= std::min(W, s2)) {
+      S = s2;
+      Wd = d;
+      break;
+    }
+  }
   W = Wd;
   std::memset(&rp, 0, offsetof(RingParams, pair_end));
   rp.x = xp;
@@ -534,7 +545,18 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
       // over up to kSmallOpCtas CTAs so they are all in flight at once; it ends within microseconds,
       // so the SM quota it briefly exceeds costs co-running work little
       const int64_t op_bytes = int64_t(p->nkv) * plan.total_tokens * p->tok_bytes * (x->layer_end - x->layer_begin);
-      if (!x->num_ctas && op_bytes < kSmallOpBytes) c = std::max(c, std::min(kSmallOpCtas, rp.npieces));
+      if (!x->num_ctas && op_bytes < kSmallOpBytes) {
+        c = std::max(c, std::min(kSmallOpCtas, rp.npieces));
+        // ... and every piece of the operation gets a stage: re-plan the rings for c CTAs with the
+        // whole operation in flight (unless the caller bounded it)
+        if (!x->inflight_kib) {
+          strata_xfer xa = *x;
+          const int64_t all = int64_t(rp.npieces) * (x->layer_end - x->layer_begin) * rp.stage_bytes;
+          xa.inflight_kib = static_cast<int32_t>(std::min<int64_t>(INT32_MAX, (all + 1023) >> 10));
+          if (!plan_ring(p, &xa, dir, xp, c, rp) || !ring_batch(p, x, plan, plan.batches[0], rp))
+            return op_fail(cudaErrorInvalidValue, "ring plan");
+        }
+      }
       rp.l0 = x->layer_begin;
       rp.l1 = x->layer_end;
       rp.epoch = static_cast<uint32_t>(t);

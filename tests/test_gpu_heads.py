@@ -162,3 +162,51 @@ def test_head_major_strided_runs_dma(H, Ht, h0, group):
         assert np.array_equal(c.pool.host, c.expected_offload(before, 0, g.L))
     finally:
         c.close()
+
+
+def test_shared_tier_outlives_first_pool():
+    """Two pools over ONE caller tier alive at once (round-1 advice): closing the pool that
+    registered it first must not unregister it under the second, whose loads keep matching the
+    oracle; a third pool whose range only partly overlaps the shared registration is refused."""
+    g_full = Geometry(L=2, H=2, D=128, e=2, P=1, C=64, num_pages=3000, num_chunks=50, Ht=2, head_major=True)
+    q = kvgen.make_requests(kvgen.rng_for(92), [2500], g_full.P, g_full.C, g_full.num_pages, g_full.num_chunks)
+    host = np.empty(g_full.host_bytes + 4096, np.uint8)
+    tier = host[:g_full.host_bytes]
+    tier[:] = kvgen.random_bytes(kvgen.rng_for(93), g_full.host_bytes)
+    import oracle
+    from tests.helpers import CANARY
+    ek = [np.full(g_full.layer_buffer_bytes, CANARY, np.uint8) for _ in range(g_full.L)]
+    ev = [np.full(g_full.layer_buffer_bytes, CANARY, np.uint8) for _ in range(g_full.L)]
+    oracle.load(g_full, tier, ek, ev, q, 0, g_full.L)
+    slots = g_full.num_pages * g_full.P
+    pools, bufs = [], []
+    for r in range(2):
+        g = dataclasses.replace(g_full, H=1, h0=r)
+        nb = g.layer_buffer_bytes
+        k = [torch.full((nb,), CANARY, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+        v = [torch.full((nb,), CANARY, dtype=torch.uint8, device="cuda") for _ in range(g.L)]
+        pools.append(st.HostPool(num_layers=g.L, num_heads=1, head_dim=g.D, elem_bytes=g.e, page_size=g.P,
+                                 chunk_tokens=g.C, k_ptrs=k, v_ptrs=v, num_pages=g.num_pages,
+                                 num_chunks=g.num_chunks, host=tier, host_heads=2, head_begin=r, head_major=True))
+        bufs.append((k, v))
+    try:
+        # a range that straddles the shared registration's end cannot share it
+        with pytest.raises(st.StrataError):
+            k, v = bufs[0]
+            st.HostPool(num_layers=g_full.L, num_heads=1, head_dim=g_full.D, elem_bytes=g_full.e, page_size=1,
+                        chunk_tokens=g_full.C, k_ptrs=k, v_ptrs=v, num_pages=g_full.num_pages,
+                        num_chunks=g_full.num_chunks, host=host[4096:4096 + g_full.host_bytes], host_heads=2,
+                        head_begin=0, head_major=True)
+        pools[0].close()
+        for _ in range(3):   # loads through the second pool after the first closed
+            pools[1].load(st.Requests.from_kvgen(q))
+        torch.cuda.synchronize()
+        k, v = bufs[1]
+        for l in range(g_full.L):
+            want_k = ek[l].reshape(slots, 2, -1)[:, 1].reshape(-1)
+            want_v = ev[l].reshape(slots, 2, -1)[:, 1].reshape(-1)
+            assert np.array_equal(k[l].cpu().numpy(), want_k)
+            assert np.array_equal(v[l].cpu().numpy(), want_v)
+    finally:
+        for p in pools:
+            p.close()

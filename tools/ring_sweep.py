@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--tag", default="")
     ap.add_argument("--layers", type=int, default=0, help="override L (0 = the config's)")
     ap.add_argument("--bulk-store", default="0", help="load: 0 st.global scatter, 1 cp.async.bulk stores (list)")
+    ap.add_argument("--inflight-kb", default="0", help="host KiB in flight over all CTAs (list; 0 = library default)")
     args = ap.parse_args()
     io = torch.cuda.Stream()
     for spec in args.configs.split(","):
@@ -72,18 +73,24 @@ def main():
         io.synchronize()
         ref = {l: (k[l].clone(), v[l].clone() if v else None) for l in check_layers}
         host_ref = pool.host.copy()
-        link = gbs(lambda: st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, k[0].data_ptr(), 0, nb, io),
-                   io, nb, 5)
-        link_d2h = gbs(lambda: st.strata_baseline_contiguous(pool.handle, st.STRATA_D2H, k[0].data_ptr(), 0, nb, io),
-                       io, nb, 5)
+        # link ceilings through a scratch buffer (not the pool's buffers: the offload check needs them)
+        scratch = torch.empty(min(nb, 256 << 20), dtype=torch.uint8, device="cuda")
+        sb = scratch.numel()
+        link = gbs(lambda: st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, sb, io),
+                   io, sb, 5)
+        link_d2h = gbs(lambda: st.strata_baseline_contiguous(pool.handle, st.STRATA_D2H, scratch.data_ptr(), 0, sb, io),
+                       io, sb, 5)
+        del scratch
         print(json.dumps({"kind": "link", "config": name, "P": g.P, "h2d_gbs": round(link, 2),
                           "d2h_gbs": round(link_d2h, 2)}), flush=True)
         for d in args.dirs.split(","):
             for c in [int(x) for x in args.ctas.split(",")]:
                 for w in [int(x) for x in (args.warps if d == "load" else args.gather_warps).split(",")]:
-                    for skb, bs in [(a_, b_) for a_ in args.stage_kb.split(",")
-                                    for b_ in (args.bulk_store.split(",") if d == "load" else ["0"])]:
+                    for skb, bs, ifk in [(a_, b_, c_) for a_ in args.stage_kb.split(",")
+                                         for b_ in (args.bulk_store.split(",") if d == "load" else ["0"])
+                                         for c_ in args.inflight_kb.split(",")]:
                         skb = int(skb)
+                        ifk = int(ifk)
                         os.environ["STRATA_RING_STAGE_KB"] = str(skb)
                         os.environ["STRATA_RING_BULK_STORE"] = bs
                         os.environ["STRATA_RING_WARPS" if d == "load" else "STRATA_RING_GATHER_WARPS"] = str(w)
@@ -92,9 +99,9 @@ def main():
                                 k[l].zero_()
                                 if v:
                                     v[l].zero_()
-                            fn = lambda: pool.load(reqs, stream=io, engine=st.STRATA_ENGINE_TMA, num_ctas=c)  # noqa: E731
+                            fn = lambda: pool.load(reqs, stream=io, engine=st.STRATA_ENGINE_TMA, num_ctas=c, inflight_kib=ifk)  # noqa: E731
                         else:
-                            fn = lambda: pool.offload(reqs, stream=io, engine=st.STRATA_ENGINE_TMA, num_ctas=c)  # noqa: E731
+                            fn = lambda: pool.offload(reqs, stream=io, engine=st.STRATA_ENGINE_TMA, num_ctas=c, inflight_kib=ifk)  # noqa: E731
                         r = gbs(fn, io, nbytes, args.reps)
                         io.synchronize()
                         if d == "load":
@@ -104,7 +111,8 @@ def main():
                             ok = bool((pool.host == host_ref).all())   # loaded from this tier: offload rewrites the same bytes
                         print(json.dumps({"kind": "ring", "tag": args.tag, "L": g.L, "flags": args.flags, "frag": args.frag,
                                           "chunk_frag": args.chunk_frag, "config": name, "P": g.P, "dir": d, "ctas": c, "warps": w,
-                                          "stage_kb": skb, "bulk_store": int(bs), "gbs": round(r, 2),
+                                          "stage_kb": skb, "bulk_store": int(bs), "inflight_kb": ifk, "gbs": round(r, 2),
+                                          "us": round(nbytes / r / 1e3, 2),
                                           "frac_link": round(r / (link if d == "load" else link_d2h), 4),
                                           "parity": ok}), flush=True)
         for key in ("STRATA_RING_STAGE_KB", "STRATA_RING_WARPS", "STRATA_RING_GATHER_WARPS", "STRATA_RING_BULK_STORE"):
