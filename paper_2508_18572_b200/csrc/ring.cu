@@ -362,7 +362,13 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(
           if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(nt * tok));
           __syncwarp();
           if (p.host_run) {
-            if (lane == 0 && nt) bulk_g2s(st, reinterpret_cast<const void*>(a), static_cast<uint32_t>(nt * tok), &full[s]);
+            if (lane == 0 && nt) {
+              if (p.debug & 2)
+                bulk_g2s_hint(st, reinterpret_cast<const void*>(a), static_cast<uint32_t>(nt * tok), &full[s],
+                              l2_policy_evict_first());
+              else
+                bulk_g2s(st, reinterpret_cast<const void*>(a), static_cast<uint32_t>(nt * tok), &full[s]);
+            }
           } else {
             for (int i = lane; i < nt; i += 32)
               bulk_g2s(st + i * tok, reinterpret_cast<const char*>(a) + int64_t(i) * x.host_tok_stride,

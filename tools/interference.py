@@ -44,6 +44,16 @@ def make_prefill():
     return run
 
 
+def make_decode1():
+    # the same 8 GiB HBM read as ONE reduction kernel (no per-layer launches): separates a memory-side
+    # slowdown from one in the launch path
+    kv = torch.randn(32 * 16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda")
+
+    def run():
+        kv.sum(dtype=torch.float32)
+    return run
+
+
 def make_decode():
     # 16 requests x 4096 tokens x 8 heads x 128 dim x bf16 x (K,V) = 256 MiB per layer, 32 layers
     kv = [torch.randn(16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda")
@@ -119,6 +129,7 @@ def main():
     ap.add_argument("--P", type=int, default=1, help="device page size")
     ap.add_argument("--flags", type=int, default=0, help="strata_pool_desc.flags of the host tier (1 = huge pages)")
     ap.add_argument("--tag", default="")
+    ap.add_argument("--proxies", default="prefill,decode", help="prefill, decode, decode1 (one-kernel decode)")
     args = ap.parse_args()
 
     g = kvgen.geometry("llama8b_32k", P=args.P, **({"L": args.layers} if args.layers else {}))
@@ -133,7 +144,8 @@ def main():
     lo, hi = torch.cuda.Stream.priority_range()
     io = torch.cuda.Stream(priority=hi)       # I/O: high priority (its few CTAs get SMs first)
     comp = torch.cuda.Stream(priority=lo)
-    proxies = {"prefill": make_prefill(), "decode": make_decode()}
+    makers = {"prefill": make_prefill, "decode": make_decode, "decode1": make_decode1}
+    proxies = {name: makers[name]() for name in args.proxies.split(",")}
     if args.graph:
         graphs = {}
         for name, fn in proxies.items():
