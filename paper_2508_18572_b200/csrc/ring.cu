@@ -523,7 +523,6 @@ cudaError_t launch_ring(const RingParams& p, int dir, int ctas, cudaStream_t s) 
   const int threads = 32 * (1 + p.warps);
   if (dir == 0) {
     if (p.x.gran == 8) return launch_k(ring_load_kernel<true, 8>, ctas, threads, smem, s, p);
-    if (p.x.gran == 4) return launch_k(ring_load_kernel<true, 4>, ctas, threads, smem, s, p);
     return contig ? launch_k(ring_load_kernel<true, 16>, ctas, threads, smem, s, p)
                   : launch_k(ring_load_kernel<false, 16>, ctas, threads, smem, s, p);
   }
@@ -536,7 +535,6 @@ cudaError_t ring_prepare(int smem) {
   if ((e = cudaFuncSetAttribute(ring_load_kernel<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(ring_load_kernel<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(ring_load_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
-  if ((e = cudaFuncSetAttribute(ring_load_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   if ((e = cudaFuncSetAttribute(ring_offload_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem))) return e;
   return cudaFuncSetAttribute(ring_offload_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }

@@ -287,7 +287,9 @@ static int env_int(const char* name, int def) {
 static bool ring_supported(const strata_pool* p, int dir) {
   if (!p->host_row_contig()) return false;
   if (p->gran == 16) return true;
-  return dir == 0 && (p->gran == 8 || p->gran == 4) && p->host_tok_stride == p->tok_bytes &&
+  // (8-byte words only: 4-byte-word rows scatter at 34.8 GB/s on the ring vs 46.6 on the narrow LDG
+  // kernel, 100-byte rows, profiles/r02/probe1/narrow.jsonl)
+  return dir == 0 && p->gran == 8 && p->host_tok_stride == p->tok_bytes &&
          (p->head_stride == p->head_bytes || p->d.num_heads == 1) &&
          reinterpret_cast<uintptr_t>(p->host_dev) % 16 == 0 && p->host_bytes % 16 == 0;
 }
