@@ -6,7 +6,12 @@ prefill and decode" (§4.2, fig:interference), from as few as one o
 engine: HBM-bound decode slows with the host reads kept in flight (no-store and exclusive-SM variants
 cost the same), and the link needs ~200 KiB in flight to run near its ceiling — measured frontier
 (profiles/r02/interference_*.jsonl): ~29 GB/s +5.6 %, ~44 +11 %, ~48.6 +12.5 %,
-~51.2 +15.6 % (LDG at 2 CTAs: 50.9 +12.1 %).  So two operating points are asserted:
+~51.2 +15.6 % (LDG at 2 CTAs: 50.9 +12.1 %).  The decode slowdown splits into a memory-side part and a per-kernel-boundary part: the same 8 GiB HBM
+read issued as 4 / 32 / 128 / 512 reduction kernels slows +6 / +17 / +103 / +163 % beside the default
+load (each kernel boundary ~20 us longer; a contiguous copy-engine memcpy: ~14 us), graph-replayed or
+not (profiles/r02/interference/decode_split_kernels.jsonl).  The memory-side part — `decode_long`,
+the read as 4 kernels — meets the paper's < 10 % at the default point.  So two operating points are
+asserted:
 
   default        the library default (ring, 2 CTAs, 224 KiB in flight): >= 85 % of the link, prefill
                  <= +5 %, decode <= +20 % (the frontier at that rate);
@@ -18,6 +23,7 @@ proxy beside a continuous load alternate for 3 rounds, 1 s idle before every blo
 
   prefill proxy  bf16 GEMMs of a Llama-3.1-8B layer for 2 x 4K tokens (tensor-core bound)
   decode proxy   a read of 16 x 4K tokens of Llama-8B KV per layer for 32 layers (HBM bound)
+  decode_long    the same 8 GiB read as 4 kernels (the memory-side interference alone)
 """
 import statistics
 import time
@@ -35,8 +41,8 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU box
 import paper_2508_18572_b200 as st  # noqa: E402
 
 POINTS = {   # operating point: (num_ctas, min fraction of the link, {proxy: max slowdown})
-    "default": (0, 0.85, {"prefill": 0.05, "decode": 0.20}),
-    "budget": (1, 0.50, {"prefill": 0.05, "decode": 0.10}),
+    "default": (0, 0.85, {"prefill": 0.05, "decode": 0.20, "decode_long": 0.10}),
+    "budget": (1, 0.50, {"prefill": 0.05, "decode": 0.10, "decode_long": 0.10}),
 }
 
 
@@ -48,8 +54,9 @@ def _prefill():
     return lambda: [torch.matmul(xs[k], w) for (k, _), w in zip(shapes, ws)]
 
 
-def _decode():
-    kv = [torch.randn(16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda") for _ in range(32)]
+def _decode(kernels=32):
+    kv = [torch.randn(32 // kernels * 16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda")
+          for _ in range(kernels)]
     return lambda: [t.sum(dtype=torch.float32) for t in kv]
 
 
@@ -68,7 +75,7 @@ def _time(fn, stream, reps=15):
 
 
 @pytest.mark.parametrize("point", ["default", "budget"])
-@pytest.mark.parametrize("proxy", ["prefill", "decode"])
+@pytest.mark.parametrize("proxy", ["prefill", "decode", "decode_long"])
 def test_interference_operating_points(proxy, point):
     ctas, min_frac, budget = POINTS[point]
     g = kvgen.geometry("llama8b_32k")
@@ -93,7 +100,7 @@ def test_interference_operating_points(proxy, point):
             b.synchronize()
             ts.append(a.elapsed_time(b))
         link = scratch.numel() / (statistics.median(ts[2:]) / 1e3) / 1e9
-        fn = _prefill() if proxy == "prefill" else _decode()
+        fn = {"prefill": _prefill, "decode": _decode, "decode_long": lambda: _decode(4)}[proxy]()
         load = lambda: pool.load(reqs, stream=io, num_ctas=ctas)  # noqa: E731
         load()
         torch.cuda.synchronize()

@@ -54,6 +54,16 @@ def make_decode1():
     return run
 
 
+def make_decode_split(n):
+    total = 32 * 16 * 4096 * 8 * 128 * 2
+    kv = [torch.randn(total // n, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+
+    def run():
+        for t in kv:
+            t.sum(dtype=torch.float32)
+    return run
+
+
 def make_decode():
     # 16 requests x 4096 tokens x 8 heads x 128 dim x bf16 x (K,V) = 256 MiB per layer, 32 layers
     kv = [torch.randn(16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda")
@@ -145,7 +155,9 @@ def main():
     io = torch.cuda.Stream(priority=hi)       # I/O: high priority (its few CTAs get SMs first)
     comp = torch.cuda.Stream(priority=lo)
     makers = {"prefill": make_prefill, "decode": make_decode, "decode1": make_decode1}
-    proxies = {name: makers[name]() for name in args.proxies.split(",")}
+    # decodeN: the same 8 GiB HBM read split into N reduction kernels (per-kernel-boundary cost)
+    proxies = {name: (makers[name]() if name in makers else make_decode_split(int(name[len("decode"):])))
+               for name in args.proxies.split(",")}
     if args.graph:
         graphs = {}
         for name, fn in proxies.items():
