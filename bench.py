@@ -228,6 +228,61 @@ def cpu_baseline(g, q, host: np.ndarray, budget_s: float = 10.0):
             "numa_node_cpus": len(node_cpus) or None}
 
 
+def interference(torch, pool, reqs, io, bytes_load, link):
+    """NEXT-1 in the bench line (fig:interference): co-running proxies
+    slowed by this workload's default load.  One alone / beside pair per proxy after a 0.5 s idle,
+    10 timed repetitions each (tests/test_gpu_interference.py runs the full 3-round protocol):
+    prefill = bf16 GEMMs of a Llama-8B layer for 2 x 4K tokens; decode = an 8 GiB HBM read of 16 x 4K
+    tokens of KV for 32 layers as 32 kernels; decode_long = the same read as 4 kernels."""
+    lo, hi = torch.cuda.Stream.priority_range()
+    comp = torch.cuda.Stream(priority=lo)
+    M = 8192
+    shapes = [(4096, 6144), (4096, 4096), (4096, 28672), (14336, 4096)]
+    xs = {k: torch.randn(M, k, dtype=torch.bfloat16, device="cuda") for k, _ in shapes}
+    ws = [torch.randn(k, n, dtype=torch.bfloat16, device="cuda") for k, n in shapes]
+    kv = torch.randn(32 * 16 * 4096 * 8 * 128 * 2, dtype=torch.bfloat16, device="cuda")
+    parts32, parts4 = kv.chunk(32), kv.chunk(4)
+    proxies = {"prefill": lambda: [torch.matmul(xs[k], w) for (k, _), w in zip(shapes, ws)],
+               "decode": lambda: [t.sum(dtype=torch.float32) for t in parts32],
+               "decode_long": lambda: [t.sum(dtype=torch.float32) for t in parts4]}
+
+    def run(fn, reps=10):
+        evs = []
+        with torch.cuda.stream(comp):
+            fn()
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(comp)
+                fn()
+                b.record(comp)
+                evs.append((a, b))
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+    out = {"method": "proxy alone vs beside back-to-back default loads on a high-priority stream; "
+                     "0.5 s idle before each block; median of 10"}
+    rates = []
+    for name, fn in proxies.items():
+        time.sleep(0.5)
+        alone = run(fn)
+        n_loads = max(2, int(alone * 12 / (bytes_load / link / 1e6)) + 2)
+        time.sleep(0.5)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(io)
+        for _ in range(n_loads):
+            pool.load(reqs, stream=io)
+        b.record(io)
+        co = run(fn)
+        b.synchronize()
+        rates.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
+        out[name] = round(co / alone - 1, 4)
+    out["load_gbs_beside"] = round(statistics.median(rates), 3)
+    out["paper_budget"] = {"prefill": 0.05, "decode": 0.10, "source": "PAPER.md:262 (H200, ~50 GB/s)"}
+    del xs, ws, kv, parts32, parts4
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -482,6 +537,8 @@ def main(argv=None):
             ee, _ = timed(fe, 3)
             others[ENGINE_NAMES[eng]] = round(bytes_step * 3 / ee / 1e9, 3)
         extras["other_engines_gbs"] = others
+        if world == 1 and bytes_step >= (1 << 30) and not args.num_ctas and not args.engine:
+            extras["interference"] = interference(torch, pool, reqs, io, bytes_step, link_h2d)
         if bytes_step < (16 << 20):
             # a small load is bound by host submission (the Python call + the library's launch work,
             # ~20 us) more than by the device: the same load captured once into a CUDA graph and
