@@ -228,8 +228,12 @@ int strata_offload(strata_pool_t p, const strata_xfer* x, strata_stream_t stream
  * reused 8 operations later; an older ticket returns STRATA_ERR_STALE_TICKET.  A layer outside the
  * operation's range returns STRATA_ERR_INVALID_ARG.  Use with cudaStreamWaitEvent /
  * cudaEventSynchronize; never destroy it.  An operation issued while its stream was being captured
- * into a CUDA graph has its events inside that graph only: wait on them from the same capture;
- * strata_layer_elapsed_ms on such a ticket returns STRATA_ERR_UNSUPPORTED.  A new operation that
+ * into a CUDA graph (CAPTURED ticket) has its own events, recorded as external event nodes of the
+ * graph: every replay signals them, so this returns the event of the LATEST replay's layer, and a
+ * captured ticket never goes stale while the pool lives (its events are destroyed with the pool).
+ * strata_wait_layer on a captured ticket from a consumer stream captured into the same graph waits
+ * on the capture-internal event instead (a graph edge; needs the ticket's ring slot not yet reused,
+ * else STRATA_ERR_STALE_TICKET).  A new operation that
  * reuses a ring slot is ordered after the slot's previous one-launch operation (whose device-side
  * layer flags it shares), so a layer event never fires before that layer's bytes landed. */
 int strata_layer_event(strata_pool_t p, uint64_t ticket, int32_t layer, strata_event_t* out);
@@ -241,7 +245,8 @@ int strata_wait_layer(strata_pool_t p, uint64_t ticket, int32_t layer, strata_st
 
 /* Milliseconds from the start of operation `ticket` (0 = latest) on its stream to the completion of
  * layer `layer` (CUDA event timing).  Blocks until that layer is complete.  Errors as
- * strata_layer_event, plus STRATA_ERR_CUDA. */
+ * strata_layer_event, plus STRATA_ERR_CUDA (also: a captured ticket whose graph has not been
+ * replayed yet; after a replay it times that replay). */
 int strata_layer_elapsed_ms(strata_pool_t p, uint64_t ticket, int32_t layer, float* ms);
 
 /* Cumulative per-pool counters since registration (observability; no synchronisation). */

@@ -156,6 +156,18 @@ int check_desc(const strata_pool_desc* d) {
   return STRATA_OK;
 }
 
+// MemAvailable from /proc/meminfo in MiB (-1 if unknown): context for an allocation failure.
+long mem_available_mb() {
+  FILE* f = fopen("/proc/meminfo", "r");
+  if (!f) return -1;
+  char line[256];
+  long kb = -1;
+  while (fgets(line, sizeof line, f))
+    if (sscanf(line, "MemAvailable: %ld kB", &kb) == 1) break;
+  fclose(f);
+  return kb < 0 ? -1 : kb / 1024;
+}
+
 // Caller memory registered by this library, shared by every pool whose tier lies inside it (e.g. one
 // host tier holding every KV head, read by the pools of several TP ranks, R28): the registration is
 // undone only when the last of those pools closes, never while another still reads it through UVA.
@@ -224,6 +236,9 @@ void destroy(strata_pool* p) {
   strata::free_fused(p);
   for (cudaEvent_t e : p->events)
     if (e) cudaEventDestroy(e);
+  for (auto& kv : p->captured_ops)
+    for (cudaEvent_t e : kv.second.ev)
+      if (e) cudaEventDestroy(e);
   if (p->bitmap) cudaFree(p->bitmap);
   if (p->err_dev) cudaFree(p->err_dev);
   if (p->err_host) cudaFreeHost(p->err_host);
@@ -346,10 +361,27 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
     pretouch(p->host, p->map_bytes);
     e = cudaHostRegister(p->host, p->map_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
     if (e != cudaSuccess) {
-      destroy(p);
-      return fail(STRATA_ERR_OOM, "cudaHostRegister(%zu): %s", p->map_bytes, cudaGetErrorString(e));
+      // page-locking the mapping failed (memory pressure / locked-memory limits): fall back to the
+      // driver's own pinned allocator before giving up
+      cudaGetLastError();
+      munmap(p->host, p->map_bytes);
+      p->host = nullptr;
+      p->host_kind = 0;
+      void* h2 = nullptr;
+      const cudaError_t e2 = cudaHostAlloc(&h2, p->host_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+      if (e2 != cudaSuccess) {
+        cudaGetLastError();
+        const size_t want = p->map_bytes;
+        const long avail_mb = mem_available_mb();
+        destroy(p);
+        return fail(STRATA_ERR_OOM, "cudaHostRegister(%zu): %s; cudaHostAlloc: %s (MemAvailable %ld MiB)", want,
+                    cudaGetErrorString(e), cudaGetErrorString(e2), avail_mb);
+      }
+      p->host = static_cast<char*>(h2);
+      p->host_kind = 2;
+    } else {
+      p->registered_by_us = true;
     }
-    p->registered_by_us = true;
   }
   void* dptr = nullptr;
   if ((e = cudaHostGetDevicePointer(&dptr, p->host, 0))) {
@@ -407,11 +439,25 @@ int strata_offload(strata_pool_t p, const strata_xfer* x, strata_stream_t stream
 }
 
 namespace {
-// Resolves (ticket, layer) to the ring slot; 0 on success.
+// A captured operation (its own events, signalled by every replay of its graph); NULL otherwise.
+const strata_pool::CapturedOp* captured_op(strata_pool_t p, uint64_t ticket) {
+  auto it = p->captured_ops.find(ticket);
+  return it == p->captured_ops.end() ? nullptr : &it->second;
+}
+
+// Resolves (ticket, layer) to the ring slot; 0 on success.  A captured ticket resolves to slot -1
+// once its ring slot has been reused (it never goes stale: its events are its own).
 int find_op(strata_pool_t p, uint64_t& ticket, int32_t layer, int& slot) {
   if (!p) return fail(STRATA_ERR_INVALID_ARG, "pool is NULL");
   const uint64_t last = p->next_ticket - 1;
   if (ticket == 0) ticket = last;
+  if (const auto* c = ticket ? captured_op(p, ticket) : nullptr) {
+    if (layer < c->l0 || layer >= c->l1)
+      return fail(STRATA_ERR_INVALID_ARG, "layer %d outside the operation's range [%d,%d)", layer, c->l0, c->l1);
+    slot = static_cast<int>(ticket % kEventRing);
+    if (p->ops[slot].ticket != ticket) slot = -1;
+    return STRATA_OK;
+  }
   if (ticket == 0 || ticket > last || ticket + kEventRing <= last)
     return fail(STRATA_ERR_STALE_TICKET, "ticket %llu not live (latest %llu, ring %d)",
                 (unsigned long long)ticket, (unsigned long long)last, kEventRing);
@@ -429,6 +475,10 @@ int strata_layer_event(strata_pool_t p, uint64_t ticket, int32_t layer, strata_e
   int slot = 0;
   int rc = find_op(p, ticket, layer, slot);
   if (rc) return rc;
+  if (const auto* c = captured_op(p, ticket)) {   // the external event every replay records
+    *out = reinterpret_cast<strata_event_t>(c->ev[size_t(1 + layer)]);
+    return STRATA_OK;
+  }
   *out = reinterpret_cast<strata_event_t>(p->events[size_t(slot) * (p->d.num_layers + 1) + 1 + layer]);
   return STRATA_OK;
 }
@@ -444,6 +494,21 @@ int strata_wait_layer(strata_pool_t p, uint64_t ticket, int32_t layer, strata_st
   int rc = find_op(p, ticket, layer, slot);
   if (rc) return rc;
   cudaError_t e;
+  if (const auto* c = captured_op(p, ticket)) {
+    // a consumer captured into the graph waits on the slot's capture-internal event (a graph edge);
+    // one outside any capture on the external event the latest replay recorded
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if ((e = cudaStreamIsCapturing(reinterpret_cast<cudaStream_t>(consumer), &cs))) return cuda_fail(e, "cudaStreamIsCapturing");
+    if (cs == cudaStreamCaptureStatusNone)
+      e = cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(consumer), c->ev[size_t(1 + layer)], 0);
+    else if (slot >= 0)
+      e = cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(consumer),
+                              p->events[size_t(slot) * (p->d.num_layers + 1) + 1 + layer], 0);
+    else
+      return fail(STRATA_ERR_STALE_TICKET, "captured ticket %llu: its ring slot was reused, so a consumer inside a "
+                  "capture can no longer depend on it (wait from outside the capture)", (unsigned long long)ticket);
+    return e == cudaSuccess ? STRATA_OK : cuda_fail(e, "cudaStreamWaitEvent");
+  }
   // a fused operation's layers (except the last, whose event the caller's stream records) are
   // waited on at their device flag directly, without the side stream's event hop
   if (p->ops[slot].fused && layer + 1 < p->ops[slot].l1) {
@@ -460,9 +525,14 @@ int strata_layer_elapsed_ms(strata_pool_t p, uint64_t ticket, int32_t layer, flo
   int slot = 0;
   int rc = find_op(p, ticket, layer, slot);
   if (rc) return rc;
-  if (p->ops[slot].captured)
-    return fail(STRATA_ERR_UNSUPPORTED, "ticket %llu was captured into a CUDA graph: its events exist only inside "
-                "that graph (time the graph's replay instead)", (unsigned long long)ticket);
+  if (const auto* c = captured_op(p, ticket)) {   // the latest replay's external events
+    cudaError_t e = cudaEventSynchronize(c->ev[size_t(1 + layer)]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(ms, c->ev[0], c->ev[size_t(1 + layer)]);
+    if (e == cudaSuccess) return STRATA_OK;
+    cudaGetLastError();   // the library's own failed call: not left pending on the caller's thread
+    return fail(STRATA_ERR_CUDA, "captured ticket %llu: %s (has its graph been replayed?)",
+                (unsigned long long)ticket, cudaGetErrorString(e));
+  }
   const size_t base = size_t(slot) * (p->d.num_layers + 1);
   cudaError_t e = cudaEventSynchronize(p->events[base + 1 + layer]);
   if (e == cudaSuccess) e = cudaEventElapsedTime(ms, p->events[base], p->events[base + 1 + layer]);

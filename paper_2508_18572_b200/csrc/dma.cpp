@@ -311,7 +311,6 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
                  int dir, int slot_ev) {
   if (!x->host_chunks_host && plan.total_tokens > 0)
     return fail(STRATA_ERR_INVALID_ARG, "STRATA_ENGINE_DMA needs xfer.host_chunks_host");
-  const int L = p->d.num_layers;
   std::vector<ChunkPos> pos;
   int rc = collect_positions(p, x, plan, pos);
   if (rc) return rc;
@@ -380,7 +379,6 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
   uint64_t capture_seq = 0;
   uint64_t& seq = capst == cudaStreamCaptureStatusActive ? capture_seq : D.seq;
   int last_slot = 0;
-  auto layer_event = [&](int32_t l) { return p->events[size_t(slot_ev) * (L + 1) + 1 + l]; };
   for (int32_t lg = x->layer_begin; lg < x->layer_end; lg += m.G) {
     const int gl = std::min<int>(m.G, x->layer_end - lg);   // layers in this group
     const std::vector<Piece>& gp = (lg == x->layer_begin || lg + m.G >= x->layer_end) ? edge_pieces : pieces;
@@ -404,7 +402,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
           if (le != cudaSuccess) return le;
           ++p->counters.kernel_launches;
           // loads: layer lg+g is complete once its scatter of the group's last piece has run
-          if (kdir == 0 && last_piece && (le = cudaEventRecord(layer_event(lg + g), s))) return le;
+          if (kdir == 0 && last_piece && (le = op_record(p, slot_ev, 1 + lg + g, s))) return le;
         }
         return cudaSuccess;
       };
@@ -446,7 +444,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
     }
     if (dir == 0 && pieces.empty()) {
       for (int g = 0; g < gl; ++g)
-        if ((e = cudaEventRecord(layer_event(lg + g), s))) return cuda_fail(e, "cudaEventRecord");
+        if ((e = op_record(p, slot_ev, 1 + lg + g, s))) return cuda_fail(e, "cudaEventRecord");
     } else if (dir == 1) {
       // host bytes of the group are written once every copy stream has passed its last piece
       if (!pieces.empty())
@@ -454,7 +452,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
           if ((e = cudaStreamWaitEvent(D.cs[0], D.ev_copy[last_slot][c], 0)))
             return cuda_fail(e, "cudaStreamWaitEvent");
       for (int g = 0; g < gl; ++g)
-        if ((e = cudaEventRecord(layer_event(lg + g), D.cs[0]))) return cuda_fail(e, "cudaEventRecord");
+        if ((e = op_record(p, slot_ev, 1 + lg + g, D.cs[0]))) return cuda_fail(e, "cudaEventRecord");
     }
   }
   if (dir == 1 && i > 0)  // join: the caller's stream is ordered after every copy

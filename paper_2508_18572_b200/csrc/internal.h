@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -174,6 +175,12 @@ struct strata_pool {
   // captured: recorded into a CUDA graph capture; its events exist only inside that graph
   struct Op { uint64_t ticket; int32_t l0, l1; bool fused = false; bool captured = false; };
   Op ops[strata::kEventRing];
+  // captured operations: their own L+1 events (start, layers), recorded as EXTERNAL event nodes so
+  // every replay of the graph signals them; kept while the pool lives (a captured ticket never goes
+  // stale), keyed by ticket.  The ring slot's events are recorded too (capture-internal: a consumer
+  // captured into the same graph waits on those, which become graph edges).
+  struct CapturedOp { int32_t l0, l1; std::vector<cudaEvent_t> ev; };
+  std::map<uint64_t, CapturedOp> captured_ops;
   uint64_t next_ticket = 1;
   // validate scratch (device)
   uint32_t* bitmap = nullptr;
@@ -294,6 +301,9 @@ int ilog2_exact(int v);                                                         
 bool dma_runs_ok(const strata_pool* p);                                                       // transfer.cpp
 uint32_t div_magic(int d, int n_max);   // m with umulhi(n, m) == n / d for n < n_max, or 0  transfer.cpp
 int transfer(strata_pool* p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir); // transfer.cpp
+// Records event `idx` (0 = start, 1 + l = layer l) of the operation in ring slot `slot` on `s`; for a
+// captured operation also its dedicated event as an external node (transfer.cpp).
+cudaError_t op_record(strata_pool* p, int slot, int idx, cudaStream_t s);
 int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, XferParams xp, cudaStream_t s,
                  int dir, int slot_ev);                                                       // dma.cpp
 void free_dma(strata_pool* p);

@@ -401,6 +401,40 @@ static cudaError_t fused_events(strata_pool* p, int slot, const strata_xfer* x, 
   return cudaSuccess;
 }
 
+cudaError_t op_record(strata_pool* p, int slot, int idx, cudaStream_t s) {
+  cudaError_t e = cudaEventRecord(p->events[size_t(slot) * (p->d.num_layers + 1) + idx], s);
+  if (e != cudaSuccess || !p->ops[slot].captured) return e;
+  auto it = p->captured_ops.find(p->ops[slot].ticket);
+  if (it == p->captured_ops.end()) return cudaErrorInvalidValue;
+  return cudaEventRecordWithFlags(it->second.ev[size_t(idx)], s, cudaEventRecordExternal);
+}
+
+// A captured operation gets its own events (external nodes of the graph, signalled by every replay).
+static cudaError_t begin_captured(strata_pool* p, uint64_t t, const strata_xfer* x) {
+  strata_pool::CapturedOp op;
+  op.l0 = x->layer_begin;
+  op.l1 = x->layer_end;
+  op.ev.assign(size_t(p->d.num_layers) + 1, nullptr);
+  for (auto& ev : op.ev) {
+    cudaError_t e = cudaEventCreate(&ev);
+    if (e != cudaSuccess) {
+      for (auto& v : op.ev)
+        if (v) cudaEventDestroy(v);
+      return e;
+    }
+  }
+  p->captured_ops[t] = std::move(op);
+  return cudaSuccess;
+}
+
+static void drop_captured(strata_pool* p, uint64_t t) {
+  auto it = p->captured_ops.find(t);
+  if (it == p->captured_ops.end()) return;
+  for (auto& v : it->second.ev)
+    if (v) cudaEventDestroy(v);
+  p->captured_ops.erase(it);
+}
+
 int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ticket, int dir) {
   if (!p) return fail(STRATA_ERR_INVALID_ARG, "pool is NULL");
   Plan plan;
@@ -466,14 +500,20 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     const int slot = static_cast<int>(t % kEventRing);
     p->ops[slot] = {t, x->layer_begin, x->layer_end};
     p->ops[slot].captured = cap != cudaStreamCaptureStatusNone;
-    e = cudaEventRecord(p->events[size_t(slot) * (p->d.num_layers + 1)], s);
+    if (p->ops[slot].captured && (e = begin_captured(p, t, x)) != cudaSuccess) {
+      p->ops[slot].ticket = 0;
+      return cuda_fail(e, "cudaEventCreate");
+    }
+    e = op_record(p, slot, 0, s);
     if (e != cudaSuccess) {
       p->ops[slot].ticket = 0;   // a failed operation has no valid events
+      drop_captured(p, t);
       return cuda_fail(e, "cudaEventRecord");
     }
     rc = transfer_dma(p, x, plan, xp, s, dir, slot);
     if (rc) {
       p->ops[slot].ticket = 0;
+      drop_captured(p, t);
       return rc;
     }
     count_op(p, plan, x, engine);
@@ -532,9 +572,11 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   // a failed operation keeps no ticket: its ring slot must not hand out stale events
   auto op_fail = [&](cudaError_t err, const char* what) {
     p->ops[slot].ticket = 0;
+    drop_captured(p, t);
     return cuda_fail(err, what);
   };
-  e = cudaEventRecord(p->events[size_t(slot) * (L + 1)], s);  // operation start
+  if (p->ops[slot].captured && (e = begin_captured(p, t, x)) != cudaSuccess) return op_fail(e, "cudaEventCreate");
+  e = op_record(p, slot, 0, s);  // operation start
   if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
   // One launch for all layers when the call is one request table and not being captured (stream
   // memory operations are not captured here); layer events come from the device flags.
@@ -586,7 +628,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
         if ((e = strata::launch_ring(rp, dir, c, s))) return op_fail(e, "ring kernel launch");
         ++p->counters.kernel_launches;
       }
-      if ((e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], s))) return op_fail(e, "cudaEventRecord");
+      if ((e = op_record(p, slot, 1 + l, s))) return op_fail(e, "cudaEventRecord");
     }
     count_op(p, plan, x, engine);
     if (ticket) *ticket = t;
@@ -645,7 +687,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
       if (e != cudaSuccess) return op_fail(e, "transfer kernel launch");
       ++p->counters.kernel_launches;
     }
-    e = cudaEventRecord(p->events[size_t(slot) * (L + 1) + 1 + l], s);
+    e = op_record(p, slot, 1 + l, s);
     if (e != cudaSuccess) return op_fail(e, "cudaEventRecord");
   }
   count_op(p, plan, x, engine);

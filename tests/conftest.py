@@ -18,3 +18,23 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture(autouse=True)
+def _release_gpu_test_memory(request):
+    """After a GPU test, collect what it left behind (host pools closed by __del__, multi-GiB numpy
+    oracle images, cached device blocks): the whole -m gpu suite runs in ONE process and the
+    full-size configs pin tens of GiB of host memory, so a later test's registration must not
+    depend on when the garbage collector happens to run."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import gc
+    gc.collect()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+    except Exception:
+        pass
