@@ -57,11 +57,14 @@ static int ensure_dma(strata_pool* p, strata_pool::DmaDir& D, size_t slot_bytes,
       D.ncs = std::max(1, std::min(strata_pool::kCopyStreams, atoi(v)));
     for (auto& c : D.cs)
       if ((e = cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking))) return cuda_fail(e, "cudaStreamCreate");
-    if ((e = cudaEventCreateWithFlags(&D.ev_fork, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+    for (cudaEvent_t* f : {&D.ev_fork, &D.cap_fork})
+      if ((e = cudaEventCreateWithFlags(f, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
     for (int s = 0; s < 2; ++s) {
-      if ((e = cudaEventCreateWithFlags(&D.ev_slot[s], cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
-      for (auto& ev : D.ev_copy[s])
-        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+      for (cudaEvent_t* f : {&D.ev_slot[s], &D.cap_slot[s]})
+        if ((e = cudaEventCreateWithFlags(f, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
+      for (int c = 0; c < strata_pool::kCopyStreams; ++c)
+        for (cudaEvent_t* f : {&D.ev_copy[s][c], &D.cap_copy[s][c]})
+          if ((e = cudaEventCreateWithFlags(f, cudaEventDisableTiming))) return cuda_fail(e, "cudaEventCreate");
     }
   }
   const bool grow_stage = D.stage_bytes < slot_bytes, grow_ids = p->slot_cap < slots;
@@ -105,11 +108,14 @@ void free_dma(strata_pool* p) {
       if (b) cudaFree(b);
     for (auto& c : D.cs)
       if (c) cudaStreamDestroy(c);
-    if (D.ev_fork) cudaEventDestroy(D.ev_fork);
+    for (cudaEvent_t ev : {D.ev_fork, D.cap_fork})
+      if (ev) cudaEventDestroy(ev);
     for (int s = 0; s < 2; ++s) {
-      if (D.ev_slot[s]) cudaEventDestroy(D.ev_slot[s]);
-      for (auto& ev : D.ev_copy[s])
+      for (cudaEvent_t ev : {D.ev_slot[s], D.cap_slot[s]})
         if (ev) cudaEventDestroy(ev);
+      for (int c = 0; c < strata_pool::kCopyStreams; ++c)
+        for (cudaEvent_t ev : {D.ev_copy[s][c], D.cap_copy[s][c]})
+          if (ev) cudaEventDestroy(ev);
     }
   }
 }
@@ -355,6 +361,20 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, strata:
                   static_cast<int64_t>(std::max<size_t>(1, stage_target / m.unit)),
                   capst == cudaStreamCaptureStatusActive);
   if (rc) return rc;
+  // a captured operation records into the capture set of events (swapped back on every exit)
+  struct CaptureEvents {
+    strata_pool::DmaDir& D;
+    bool on;
+    void swap() {
+      std::swap(D.ev_fork, D.cap_fork);
+      for (int s = 0; s < 2; ++s) {
+        std::swap(D.ev_slot[s], D.cap_slot[s]);
+        for (int c = 0; c < strata_pool::kCopyStreams; ++c) std::swap(D.ev_copy[s][c], D.cap_copy[s][c]);
+      }
+    }
+    CaptureEvents(strata_pool::DmaDir& d, bool capturing) : D(d), on(capturing) { if (on) swap(); }
+    ~CaptureEvents() { if (on) swap(); }
+  } capture_events(D, capst == cudaStreamCaptureStatusActive);
 
   cudaError_t e;
   const int threads = x->threads ? x->threads : kDefaultThreadsLdg;

@@ -206,6 +206,11 @@ struct strata_pool {
     cudaEvent_t ev_fork = nullptr;
     cudaEvent_t ev_slot[2] = {nullptr, nullptr};   // staging slot reusable
     cudaEvent_t ev_copy[2][kCopyStreams] = {};     // a slot's copies done, per stream
+    // a second set of the three above, swapped in while an operation is being captured: records
+    // made inside a capture must not become the 'latest record' a later live operation waits on
+    cudaEvent_t cap_fork = nullptr;
+    cudaEvent_t cap_slot[2] = {nullptr, nullptr};
+    cudaEvent_t cap_copy[2][kCopyStreams] = {};
     uint64_t seq = 0;                 // pieces issued in this direction so far
     bool captured = false;            // a graph captured this direction: its buffers must not move
   } dma[2];
