@@ -27,7 +27,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def main():
     lib = ctypes.CDLL(os.path.join(HERE, "probe", "libchase.so"))
-    lib.chase_launch.argtypes = [ctypes.c_void_p, ctypes.c_uint, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]
+    lib.chase_launch.argtypes = [ctypes.c_void_p, ctypes.c_uint, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.c_int]
     slots = (512 << 20) // 128
     perm = np.random.default_rng(5).permutation(slots).astype(np.uint32)
     nxt = np.empty(slots, np.uint32)
@@ -50,19 +51,29 @@ def main():
     scratch = torch.empty(128 << 20, dtype=torch.uint8, device="cuda")
     steps = 20000
 
-    def chase_ns():
-        lib.chase_launch(d_next.data_ptr(), int(perm[0]), steps, out.data_ptr(), probe.cuda_stream)
-        probe.synchronize()
-        cyc = int(out[0].item())
-        return cyc / steps / (1965e6 / 1e9)            # cycles at the max SM clock -> ns (clocks sampled by bench)
-
-    def empty_chain_us(n=200):
+    def chase_ns(smem):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        x = torch.zeros(1, device="cuda")
+        a.record(probe)
+        lib.chase_launch(d_next.data_ptr(), int(perm[0]), steps, out.data_ptr(), probe.cuda_stream, smem)
+        b.record(probe)
+        probe.synchronize()
+        return a.elapsed_time(b) * 1e6 / steps          # wall ns per dependent access (incl. one launch)
+
+    # a chain of 500 one-element kernels captured in a CUDA graph: device-side launch cadence
+    x = torch.zeros(1, device="cuda")
+    chain = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(probe):
+        x.add_(1)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(chain, stream=probe):
+            for _ in range(500):
+                x.add_(1)
+
+    def empty_chain_us(n=500):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(probe):
             a.record(probe)
-            for _ in range(n):
-                x.add_(1)
+            chain.replay()
             b.record(probe)
         b.synchronize()
         return a.elapsed_time(b) * 1e3 / n
@@ -76,21 +87,22 @@ def main():
         else:
             c = {"ring_default": 0, "ring_1cta": 1}[kind]
             fn = lambda: pool.load(reqs, stream=io, num_ctas=c)  # noqa: E731
-        res = {"beside": kind, "chase_ns": [], "empty_kernel_us": []}
+        res = {"beside": kind, "chase_ns": [], "chase_ns_own_sm": [], "empty_kernel_us": []}
         for _ in range(5):
             if fn:
                 for _ in range(3):
                     fn()
-            res["chase_ns"].append(chase_ns())
+            res["chase_ns"].append(chase_ns(0))
+            res["chase_ns_own_sm"].append(chase_ns(200 << 10))
             res["empty_kernel_us"].append(empty_chain_us())
             torch.cuda.synchronize()
-        res["chase_ns_median"] = round(statistics.median(res["chase_ns"]), 1)
-        res["empty_kernel_us_median"] = round(statistics.median(res["empty_kernel_us"]), 2)
-        res["chase_ns"] = [round(x, 1) for x in res["chase_ns"]]
-        res["empty_kernel_us"] = [round(x, 2) for x in res["empty_kernel_us"]]
+        for key in ("chase_ns", "chase_ns_own_sm", "empty_kernel_us"):
+            res[key + "_median"] = round(statistics.median(res[key]), 2)
+            res[key] = [round(v, 2) for v in res[key]]
         return res
 
-    chase_ns()
+    chase_ns(0)
+    chase_ns(200 << 10)
     for kind in ("alone", "ring_default", "ring_1cta", "memcpy", "alone"):
         print(json.dumps(beside(kind)), flush=True)
     pool.close()

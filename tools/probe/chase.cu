@@ -18,8 +18,13 @@ __global__ void chase_kernel(const uint32_t* next, uint32_t start, int64_t steps
 }
 
 // launches one chase on `stream`; out[0] = SM cycles for `steps` dependent loads
-extern "C" int chase_launch(const void* next, unsigned start, long long steps, void* out, void* stream) {
-  chase_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint32_t*>(next), start, steps,
-                                                                static_cast<uint64_t*>(out));
+// smem_bytes > 0: the chase CTA requests that much dynamic shared memory, so it cannot share an SM
+// with a ring CTA (which holds ~115 KiB) — separates a GPU-wide effect from SM co-location
+extern "C" int chase_launch(const void* next, unsigned start, long long steps, void* out, void* stream,
+                            int smem_bytes) {
+  if (smem_bytes > 48 * 1024)
+    cudaFuncSetAttribute(chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  chase_kernel<<<1, 1, smem_bytes, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint32_t*>(next), start,
+                                                                         steps, static_cast<uint64_t*>(out));
   return static_cast<int>(cudaGetLastError());
 }
