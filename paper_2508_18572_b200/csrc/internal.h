@@ -283,7 +283,12 @@ constexpr int kDefaultCtasTma = 2;   // STRATA_ENGINE_TMA_BULK (scaled up for sm
 // need 4 (2 CTAs: 43.8 / 40.1).  One CTA tops out at ~36-39 GB/s: the SM's L1->XBAR request path
 // (profiles/r02/ncu_ring_load_1cta_v4.txt).
 constexpr int kDefaultCtasRingLoad = 2;
-constexpr int kDefaultCtasRingOffload = 2;
+// Offloads: 4 CTAs.  The cp.async gathers of a large, randomly paged pool keep 2 CTAs below the link
+// (Qwen-14B batch, 70 GiB pool: 49.8 GB/s from 2 CTAs, 52.7 from 3 or 4; 1152-byte MLA rows 48.0 vs
+// 52.1; Llama-8B 52.2-52.6 either way: profiles/r02/probe2/sweep_qwen_off.jsonl, sweep70/, probe4/).
+// The paper gives backups one block as a non-critical path; on B200 the SM count of
+// the I/O kernel does not move the co-runners' slowdown, the bytes in flight do.
+constexpr int kDefaultCtasRingOffload = 4;
 constexpr int kRingSmallRowBytes = 1024;   // rows below this take twice the quota
 constexpr int64_t kSmallOpBytes = int64_t(16) << 20;   // ring operations below this: all pieces in flight
 constexpr int kSmallOpCtas = 16;

@@ -523,10 +523,9 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   RingParams rp;
   int ctas = x->num_ctas;
   if (engine == STRATA_ENGINE_TMA) {
-    // rows below kRingSmallRowBytes (loads) / kRingShortRowBytes (offloads: the cp.async gather of
-    // 1152-byte MLA rows moves 48.0 GB/s from 2 CTAs, 52.1 from 4; profiles/r02/sweep70/) take twice the quota
-    const int c = ctas ? ctas : (dir == 0 ? kDefaultCtasRingLoad : kDefaultCtasRingOffload) *
-                                    (p->tok_bytes < (dir == 0 ? kRingSmallRowBytes : kRingShortRowBytes) ? 2 : 1);
+    // load rows below kRingSmallRowBytes take twice the quota (256-byte rows: 43.8 GB/s from 2 CTAs)
+    const int c = ctas ? ctas : dir == 0 ? kDefaultCtasRingLoad * (p->tok_bytes < kRingSmallRowBytes ? 2 : 1)
+                                         : kDefaultCtasRingOffload;
     if (!(ring_supported(p, dir) && plan_ring(p, x, dir, xp, c, rp))) engine = STRATA_ENGINE_LDG;
     else ctas = c;
   }

@@ -51,10 +51,18 @@ def main():
     scratch = torch.empty(128 << 20, dtype=torch.uint8, device="cuda")
     steps = 20000
 
-    def chase_ns(smem):
+    cursor = [1]
+
+    def chase_ns(smem, fresh=False):
+        """fresh=False: the same 20000-line path every call (L2-resident after the first: L2-hit
+        latency); fresh=True: the next 20000 lines of the 4M-line cycle (HBM-miss latency)."""
+        start = int(perm[0])
+        if fresh:
+            start = int(perm[(cursor[0] * steps) % slots])
+            cursor[0] += 1
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(probe)
-        lib.chase_launch(d_next.data_ptr(), int(perm[0]), steps, out.data_ptr(), probe.cuda_stream, smem)
+        lib.chase_launch(d_next.data_ptr(), start, steps, out.data_ptr(), probe.cuda_stream, smem)
         b.record(probe)
         probe.synchronize()
         return a.elapsed_time(b) * 1e6 / steps          # wall ns per dependent access (incl. one launch)
@@ -85,25 +93,27 @@ def main():
             fn = lambda: [st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0,  # noqa: E731
                                                         scratch.numel(), io) for _ in range(16)]
         else:
-            c = {"ring_default": 0, "ring_1cta": 1}[kind]
-            fn = lambda: pool.load(reqs, stream=io, num_ctas=c)  # noqa: E731
-        res = {"beside": kind, "chase_ns": [], "chase_ns_own_sm": [], "empty_kernel_us": []}
+            c = {"ring_default": 0, "ring_1cta": 1, "ldg_2cta": 2}[kind]
+            eng = st.STRATA_ENGINE_LDG if kind.startswith("ldg") else 0
+            fn = lambda: pool.load(reqs, stream=io, num_ctas=c, engine=eng)  # noqa: E731
+        res = {"beside": kind, "chase_ns": [], "chase_ns_own_sm": [], "hbm_chase_ns_own_sm": [], "empty_kernel_us": []}
         for _ in range(5):
             if fn:
                 for _ in range(3):
                     fn()
             res["chase_ns"].append(chase_ns(0))
             res["chase_ns_own_sm"].append(chase_ns(200 << 10))
+            res["hbm_chase_ns_own_sm"].append(chase_ns(200 << 10, fresh=True))
             res["empty_kernel_us"].append(empty_chain_us())
             torch.cuda.synchronize()
-        for key in ("chase_ns", "chase_ns_own_sm", "empty_kernel_us"):
+        for key in ("chase_ns", "chase_ns_own_sm", "hbm_chase_ns_own_sm", "empty_kernel_us"):
             res[key + "_median"] = round(statistics.median(res[key]), 2)
             res[key] = [round(v, 2) for v in res[key]]
         return res
 
     chase_ns(0)
     chase_ns(200 << 10)
-    for kind in ("alone", "ring_default", "ring_1cta", "memcpy", "alone"):
+    for kind in ("alone", "ring_default", "ring_1cta", "memcpy", "ldg_2cta", "alone"):
         print(json.dumps(beside(kind)), flush=True)
     pool.close()
 
