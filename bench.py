@@ -492,23 +492,44 @@ def main(argv=None):
     extras = {}
     if not args.no_extras:
         n_x = max(3, min(args.steps, 10))
-        # the same workload at page size 16 (the target holds at P = 1 and 16): a second
-        # pool over the same device buffers and host tier, P=16 page tables
-        g16, q16 = workload(args, rank, world, P=16)
-        assert g16.num_pages * 16 <= g.num_pages * g.P, "P=16 pool must fit the device buffers"
-        pool16 = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=16,
-                             chunk_tokens=g.C, k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=g16.num_pages,
-                             num_chunks=g.num_chunks, device=local, host_heads=g.Ht, head_begin=g.h0,
-                             head_major=g.head_major, host=pool.host)
-        reqs16 = st.Requests.from_kvgen(q16, device=local)
-        f16 = lambda: pool16.load(reqs16, 0, g.L, stream=io, engine=args.engine, num_ctas=args.num_ctas)  # noqa: E731
-        f16()
-        barrier()
-        e16, _ = timed(f16, n_x)
-        pr16 = scale_record(gather_floats(dist, world, [e16, link_h2d], red_dev), bytes_step, n_x)
-        extras["page_size_16"] = {"value": round(pr16["value"], 3), "frac_of_link": pr16["min_frac_over_ranks"],
-                                  "steps": n_x, "engine": ENGINE_NAMES.get(pool16.counters()["last_engine"])}
-        pool16.close()
+        # the same workload at page sizes 2..64 (the metric's "page sizes 1-64"; the target
+        # holds at P = 1 and 16): a second pool over the same device buffers and host tier per P
+        sweep = {}
+        for Pv in (2, 4, 8, 16, 32, 64):
+            if Pv == g.P:
+                continue
+            gP, qP = workload(args, rank, world, P=Pv)
+            if gP.num_pages * Pv > g.num_pages * g.P:
+                continue   # the pool would not fit the device buffers
+            poolP = st.HostPool(num_layers=g.L, num_heads=g.H, head_dim=g.D, elem_bytes=g.e, page_size=Pv,
+                                chunk_tokens=g.C, k_ptrs=k, v_ptrs=v if g.kv == 2 else None, num_pages=gP.num_pages,
+                                num_chunks=g.num_chunks, device=local, host_heads=g.Ht, head_begin=g.h0,
+                                head_major=g.head_major, host=pool.host)
+            reqsP = st.Requests.from_kvgen(qP, device=local)
+            fP = lambda: poolP.load(reqsP, 0, g.L, stream=io, engine=args.engine, num_ctas=args.num_ctas)  # noqa: E731
+            fP()
+            barrier()
+            eP, _ = timed(fP, n_x if Pv == 16 else 3)
+            prP = scale_record(gather_floats(dist, world, [eP, link_h2d], red_dev), bytes_step, n_x if Pv == 16 else 3)
+            sweep[Pv] = {"value": round(prP["value"], 3), "frac_of_link": prP["min_frac_over_ranks"],
+                         "steps": n_x if Pv == 16 else 3,
+                         "engine": ENGINE_NAMES.get(poolP.counters()["last_engine"])}
+            if Pv == 32 and world == 1:
+                # the paper's fragmentation baseline at SGLang-HiCache's page size:
+                # one cudaMemcpyAsync per (layer, K|V, page) from the same tier, host wall clock to completion
+                xb = reqsP.xfer(0, g.L, host_lists=True)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ncalls = st.strata_baseline_memcpy_pages(poolP.handle, xb, st.STRATA_H2D, io)
+                io.synchronize()
+                tb = time.perf_counter() - t0
+                extras["per_page_memcpy_baseline_P32"] = {
+                    "value": round(bytes_step / tb / 1e9, 3), "frac_of_link": round(bytes_step / tb / 1e9 / link_h2d, 4),
+                    "cudaMemcpyAsync_calls": ncalls, "wall_s": round(tb, 3),
+                    "paper": "~22 % of PCIe 5.0 for per-page DMA at P = 32 (PAPER.md:182, H200)"}
+            poolP.close()
+        extras["page_size_16"] = sweep.get(16)
+        extras["page_size_sweep"] = {"P=%d" % k_: v_ for k_, v_ in sorted(sweep.items())}
         # offload (write-back) of the same workload at its default quota vs the D2H link
         fo = lambda: pool.offload(reqs, 0, g.L, stream=io)  # noqa: E731
         fo()
