@@ -36,6 +36,9 @@ def main():
     ap.add_argument("--load-engine", type=int, default=0)
     ap.add_argument("--offload-engine", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--grid", default="",
+                    help="load+offload operating points 'load_ctas:load_inflight_kib:off_ctas:off_inflight_kib,...' "
+                         "(0 = library default), measured after the two one-direction runs")
     args = ap.parse_args()
     base = kvgen.geometry(args.config)
     n = args.tokens or kvgen.CONFIGS[args.config]["n"][0]
@@ -56,16 +59,16 @@ def main():
     nbytes = 2 * g.L * n * g.token_bytes
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
 
-    def run(which):
+    def run(which, lc=0, li=0, oc=0, oi=0):
         torch.cuda.synchronize()
         a0, a1, b0, b1 = ev(), ev(), ev(), ev()
         if "load" in which:
             a0.record(sa)
-            pool.load(ra, stream=sa, engine=args.load_engine)
+            pool.load(ra, stream=sa, engine=args.load_engine, num_ctas=lc, inflight_kib=li)
             a1.record(sa)
         if "offload" in which:
             b0.record(sb)
-            pool.offload(rb, stream=sb, engine=args.offload_engine)
+            pool.offload(rb, stream=sb, engine=args.offload_engine, num_ctas=oc, inflight_kib=oi)
             b1.record(sb)
         torch.cuda.synchronize()
         out = {}
@@ -75,17 +78,36 @@ def main():
             out["offload_ms"] = b0.elapsed_time(b1)
         return out
 
+    solo_gbs = {}
+
     def med(rs, key):
         return statistics.median(r[key] for r in rs)
 
-    for which in (("load",), ("offload",), ("load", "offload")):
-        run(which)
-        rs = [run(which) for _ in range(args.reps)]
-        rec = {"config": args.config, "tokens_per_direction": n, "bytes_per_direction": nbytes, "mode": "+".join(which)}
+    points = [(w, (0, 0, 0, 0)) for w in (("load",), ("offload",), ("load", "offload"))]
+    if args.grid:
+        points = points[:2] + [(("load", "offload"), tuple(int(v) for v in spec.split(":"))) for spec in args.grid.split(",")]
+    for which, knobs in points:
+        run(which, *knobs)
+        rs = [run(which, *knobs) for _ in range(args.reps)]
+        rec = {"config": args.config, "tokens_per_direction": n, "bytes_per_direction": nbytes, "mode": "+".join(which),
+               "load_ctas": knobs[0], "load_inflight_kib": knobs[1], "offload_ctas": knobs[2],
+               "offload_inflight_kib": knobs[3]}
         for key in ("load_ms", "offload_ms"):
             if key in rs[0]:
                 rec[key] = round(med(rs, key), 3)
                 rec[key.replace("_ms", "_gbs")] = round(nbytes / (med(rs, key) / 1e3) / 1e9, 2)
+        if len(which) == 2:
+            # rates while BOTH run: the direction that finishes first ran alone for none of its time; the
+            # other moved the rest of its bytes alone afterwards at its solo rate (measured above or 51)
+            t_a, t_b = rec["load_ms"], rec["offload_ms"]
+            first, t_first, t_second = ("offload", t_b, t_a) if t_b <= t_a else ("load", t_a, t_b)
+            solo = solo_gbs.get("load" if first == "offload" else "offload", 51.0)
+            moved_alone = solo * (t_second - t_first) / 1e3 * 1e9
+            rec["overlap_gbs"] = {first: round(nbytes / (t_first / 1e3) / 1e9, 2),
+                                  ("load" if first == "offload" else "offload"):
+                                      round(max(0.0, nbytes - moved_alone) / (t_first / 1e3) / 1e9, 2)}
+        else:
+            solo_gbs[which[0]] = rec[which[0] + "_gbs"]
         print(json.dumps(rec), flush=True)
 
     # concurrent contiguous memcpy ceiling from the same host tier
