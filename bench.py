@@ -39,8 +39,9 @@ METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 ENGINE_NAMES = {0: "default", 1: "ldg", 2: "ring", 3: "tma_bulk", 4: "dma"}
 PATH_DESC = {
     "ring": "ring_load_kernel (csrc/ring.cu): ONE persistent launch for all layers; per CTA a TMA producer warp "
-            "(one cp.async.bulk per page-first host run of <= 32 KiB, from the UVA-mapped tier) + 8 LSU scatter "
-            "warps (16-byte st.global to the pages); per-layer completion flags -> layer events",
+            "(one cp.async.bulk per page-first host run of <= 16 KiB, from the UVA-mapped tier, into a 7-stage "
+            "shared-memory ring) + up to 8 LSU scatter warps (16-byte st.global to the pages); per-layer completion "
+            "flags -> layer events",
     "ldg": "ldg_fused_kernel (csrc/kernels.cu): zero-copy 16-byte LDG/STG register staging, one launch for all layers",
     "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (one cudaMemcpyAsync per run) into an HBM "
            "staging slot + ldg_kernel scatter to the pages",
