@@ -122,6 +122,8 @@ struct RingParams {
   int32_t smem_reserve;         // > 0: dynamic shared memory to request (>= the ring's): keeps the SM exclusive
   uint32_t word_magic;          // narrow rows: row of word v < R*tok/gran = umulhi(v, magic) (0: divide)
   int32_t debug;                // A/B experiments only (env STRATA_RING_DEBUG): bit 0 = skip the page writes
+  int32_t pace_ps_per_byte;     // offload: while ring loads run on the device, this CTA issues its host
+                                // stores at most one byte per pace_ps_per_byte ps (0 = unpaced)
   int32_t pair_end[kMaxReqsPerLaunch];   // inclusive prefix sums of chunk positions per request
   char* kb[kMaxFusedLayers];    // per-layer K / V bases
   char* vb[kMaxFusedLayers];
@@ -289,6 +291,13 @@ constexpr int kDefaultCtasRingLoad = 2;
 // The paper gives backups one block as a non-critical path; on B200 the SM count of
 // the I/O kernel does not move the co-runners' slowdown, the bytes in flight do.
 constexpr int kDefaultCtasRingOffload = 4;
+// While ring loads run on the device, offloads pace themselves to this many GB/s in total
+// (RingParams::pace_ps_per_byte; 0 = unpaced).  A load and an unpaced offload in flight together
+// leave the load 15 GB/s (the offload's posted writes crowd out its read requests; waiting for store
+// completion does not help); paced to 16 GB/s the load keeps 48.7 of its 51.2 GB/s while the backup
+// continues — the backup is the non-critical path.  Offloads alone are not paced.
+// (profiles/r02/bidir/pacing/)
+constexpr int kDefaultOffloadShareGBs = 16;
 constexpr int kRingSmallRowBytes = 1024;   // rows below this take twice the quota
 constexpr int64_t kSmallOpBytes = int64_t(16) << 20;   // ring operations below this: all pieces in flight
 constexpr int kSmallOpCtas = 16;

@@ -37,6 +37,10 @@ using namespace dev;
 constexpr int kRingBarBytes = 2 * kRingMaxStages * 8 + kRingMaxStages * 4;   // full[16], empty[16], pad[16]
 constexpr int kU = 4;                                   // 16-byte vectors in flight per scatter lane
 
+// Ring-load CTAs running on this device (all pools of the process): offloads yield the host link to
+// loads while it is non-zero (RingParams::yield_k).
+__device__ unsigned int g_loads_active;
+
 // [full[16] | empty[16] | pad[16] (narrow rows: host-run offset in its 16-byte unit) | pad to 128 | S stages]
 __host__ __device__ constexpr int ring_buf_offset() { return (kRingBarBytes + 127) / 128 * 128; }
 
@@ -321,6 +325,7 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(
     }
     mbar_init_fence();
   }
+  if (threadIdx.x == 0) atomicAdd(&g_loads_active, 1u);
   __syncthreads();
   const int32_t mine = p.npieces > b ? (p.npieces - 1 - b) / G + 1 : 0;   // this CTA's pieces per layer
 
@@ -417,6 +422,8 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_load_kernel(
       }
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicSub(&g_loads_active, 1u);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -449,6 +456,7 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
   if (warp == 0) {
     // ---------------- store: stage -> host run ----------------
     uint32_t q = 0, released = 0;
+    uint64_t next_ns = 0;   // pacing: earliest issue time of the next store while a load runs
     for (int l = p.l0; l < p.l1; ++l) {
       for (int32_t m0 = 0; m0 < mine; m0 += 32) {
         const int32_t m = m0 + lane;
@@ -466,6 +474,18 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
           const uint64_t a = __shfl_sync(kFull, reinterpret_cast<uint64_t>(dst), t);
           const int nt = __shfl_sync(kFull, n, t);
           mbar_wait(&full[s], (q / S) & 1);
+          if (p.pace_ps_per_byte > 0 && *reinterpret_cast<volatile unsigned int*>(&g_loads_active) > 0) {
+            // a ring load is running on this device: the backup (a non-critical path)
+            // paces its host stores to its share of the link instead of crowding out the load
+            uint64_t now = globaltimer_ns();
+            if (next_ns > now) {
+              do {
+                __nanosleep(256);
+                now = globaltimer_ns();
+              } while (now < next_ns);
+            }
+            next_ns = now + (static_cast<uint64_t>(nt) * tok * p.pace_ps_per_byte) / 1000;
+          }
           fence_proxy_async_smem();   // the gather's cp.async (generic proxy) writes -> the bulk store
           const unsigned char* st = buf + static_cast<size_t>(s) * SB;
           if (p.host_run) {

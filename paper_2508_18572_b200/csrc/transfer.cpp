@@ -348,6 +348,11 @@ static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const
   rp.host_run = p->host_tok_stride == p->tok_bytes;
   rp.bulk_store = dir == 0 && env_int("STRATA_RING_BULK_STORE", 0) != 0;
   rp.debug = env_int("STRATA_RING_DEBUG", 0);
+  {
+    // the offload's share of the link while loads run, split over its CTAs: ps per byte per CTA
+    const int share = dir == 1 ? env_int("STRATA_OFFLOAD_SHARE_GBS", kDefaultOffloadShareGBs) : 0;
+    rp.pace_ps_per_byte = share > 0 ? static_cast<int32_t>(1000LL * std::max(1, ctas) / share) : 0;
+  }
   if (env_int("STRATA_RING_EXCLUSIVE", kDefaultRingExclusive)) rp.smem_reserve = p->tma_smem;
   if (p->gran < 16) rp.word_magic = div_magic(tok / p->gran, R * (tok / p->gran) + 32 * 4 * 32);
   for (int l = 0; l < p->d.num_layers; ++l) {
