@@ -140,6 +140,7 @@ def main():
     ap.add_argument("--flags", type=int, default=0, help="strata_pool_desc.flags of the host tier (1 = huge pages)")
     ap.add_argument("--tag", default="")
     ap.add_argument("--proxies", default="prefill,decode", help="prefill, decode, decode1 (one-kernel decode)")
+    ap.add_argument("--offload", type=int, default=0, help="1: co-run offloads (write-back) instead of loads")
     args = ap.parse_args()
 
     g = kvgen.geometry("llama8b_32k", P=args.P, **({"L": args.layers} if args.layers else {}))
@@ -184,7 +185,8 @@ def main():
                 for _ in range(g.L):
                     st.strata_baseline_contiguous(pool.handle, st.STRATA_H2D, scratch.data_ptr(), 0, scratch.numel(), io)
             return run
-        return lambda: pool.load(reqs, stream=io, engine=eng, num_ctas=c, layer_group=G)
+        op = pool.offload if args.offload else pool.load
+        return lambda: op(reqs, stream=io, engine=eng, num_ctas=c, layer_group=G)
 
     configs = []
     for eng in [int(x) for x in args.engines.split(",")]:
@@ -247,7 +249,7 @@ def main():
                     b.synchronize()
                     io_cos.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
                 al, co = statistics.median(alone_ms), statistics.median(co_ms)
-                print(json.dumps({"kind": "corun", "tag": args.tag, "L": g.L, "P": g.P, "flags": args.flags,
+                print(json.dumps({"kind": "corun", "tag": args.tag, "dir": "offload" if args.offload else "load", "L": g.L, "P": g.P, "flags": args.flags,
                                   "graph": args.graph, "engine": eng, "ctas": c, "layer_group": G, "env": env,
                                   "proxy": name, "proxy_alone_ms": round(al, 4), "proxy_corun_ms": round(co, 4),
                                   "slowdown": round(co / al - 1, 4),
