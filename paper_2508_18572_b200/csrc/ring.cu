@@ -474,17 +474,19 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
           const uint64_t a = __shfl_sync(kFull, reinterpret_cast<uint64_t>(dst), t);
           const int nt = __shfl_sync(kFull, n, t);
           mbar_wait(&full[s], (q / S) & 1);
-          if (p.pace_ps_per_byte > 0 && *reinterpret_cast<volatile unsigned int*>(&g_loads_active) > 0) {
-            // a ring load is running on this device: the backup (a non-critical path)
-            // paces its host stores to its share of the link instead of crowding out the load
-            uint64_t now = globaltimer_ns();
-            if (next_ns > now) {
-              do {
+          if (p.pace_ps_per_byte > 0) {
+            // while a ring load runs on this device the backup (a non-critical path)
+            // paces its host stores to its share of the link instead of crowding out the load;
+            // lane 0 decides and waits, the warp follows
+            if (lane == 0 && *reinterpret_cast<volatile unsigned int*>(&g_loads_active) > 0) {
+              uint64_t now = globaltimer_ns();
+              while (now < next_ns) {
                 __nanosleep(256);
                 now = globaltimer_ns();
-              } while (now < next_ns);
+              }
+              next_ns = now + (static_cast<uint64_t>(nt) * tok * p.pace_ps_per_byte) / 1000;
             }
-            next_ns = now + (static_cast<uint64_t>(nt) * tok * p.pace_ps_per_byte) / 1000;
+            __syncwarp();
           }
           fence_proxy_async_smem();   // the gather's cp.async (generic proxy) writes -> the bulk store
           const unsigned char* st = buf + static_cast<size_t>(s) * SB;
