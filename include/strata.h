@@ -49,9 +49,9 @@
  *
  * ENVIRONMENT (defaults are the measured choices of DESIGN.md §6; the knobs exist for A/B runs):
  *   STRATA_VALIDATE=1          as the STRATA_VALIDATE pool flag, for every pool
- *   STRATA_RING_INFLIGHT_KB=n  ring: host bytes in flight over all CTAs, KiB (default 224)
+ *   STRATA_RING_INFLIGHT_KB=n  ring: host bytes in flight over all CTAs, KiB (default 224; 320 for rows < 2 KiB)
  *   STRATA_RING_STAGE_KB=n     ring: piece size (default 16)
- *   STRATA_RING_WARPS=n        ring: scatter warps per load CTA (default 8; STRATA_RING_GATHER_WARPS for offloads, 4)
+ *   STRATA_RING_WARPS=n        ring: scatter warps per load CTA (default 8; STRATA_RING_GATHER_WARPS for offloads, 8)
  *   STRATA_RING_SMEM_KB=n      ring: cap on a CTA's shared memory
  *   STRATA_RING_EXCLUSIVE=1    ring: a CTA reserves its SM's shared memory (no co-resident CTAs)
  *   STRATA_RING_BULK_STORE=1   ring loads: page writes as cp.async.bulk stores instead of st.global
@@ -161,8 +161,10 @@ typedef struct {
   int32_t layer_begin;            /* l0, half-open layer range [l0, l1) (R11) */
   int32_t layer_end;              /* l1, 0 <= l0 <= l1 <= L */
   int32_t engine;                 /* strata_engine */
-  int32_t num_ctas;               /* SM quota; 0 = library default (ring: 2 CTAs,
-                                     4 for rows < 1 KiB; LDG: 2 for loads, 1 for offloads) */
+  int32_t num_ctas;               /* SM quota; 0 = library default (ring loads:
+                                     2 CTAs, 4 for rows < 1 KiB; ring offloads: 4; operations below
+                                     16 MiB: up to 16, every piece in flight; LDG: 2 for loads, 1
+                                     for offloads) */
   int32_t threads;                /* threads per CTA for STRATA_ENGINE_LDG; 0 = default */
   const int64_t* num_tokens;      /* [R] host: tokens to move per request (>= 0) */
   const int32_t* host_chunks;     /* device int32: all requests' chunk lists concatenated */
@@ -181,7 +183,8 @@ typedef struct {
                                      then completes with its group [l0 + G*k, l0 + G*(k+1)), i.e.
                                      coarser overlap for larger copies.  0 or 1 = per layer. */
   int32_t inflight_kib;           /* ring engine: host bytes kept in flight over all CTAs, in KiB
-                                     (0 = library default, 224).  The interference knob of
+                                     (0 = library default: 224, 320 for rows < 2 KiB).  The
+                                     interference knob of
                                      PAPER.md:257-262 beside num_ctas: co-running HBM-bound work slows
                                      with the host reads queued, not with the SMs used.
                                      Ignored by the other engines. */
