@@ -55,6 +55,9 @@
  *   STRATA_RING_SMEM_KB=n      ring: cap on a CTA's shared memory
  *   STRATA_RING_EXCLUSIVE=1    ring: a CTA reserves its SM's shared memory (no co-resident CTAs)
  *   STRATA_RING_BULK_STORE=1   ring loads: page writes as cp.async.bulk stores instead of st.global
+ *   STRATA_RING_STAGES=n       ring: cap on the stages per CTA
+ *   STRATA_RING_DEBUG=bits     A/B only: 1 = ring loads skip the page writes, 2 = evict-first L2
+ *                              policy on the ring's host reads
  *   STRATA_OFFLOAD_SHARE_GBS=n ring offloads pace their host stores to n GB/s in total while ring
  *                              loads run on the device (default 16; 0 = unpaced)
  *   STRATA_LDG_FUSED=0|force   per-layer launches only (LDG and ring) | fuse even 1-CTA LDG grids
