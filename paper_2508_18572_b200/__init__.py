@@ -24,12 +24,13 @@ from ._lib import (STRATA_D2H, STRATA_ENGINE_DEFAULT, STRATA_ENGINE_LDG, STRATA_
                    STRATA_ENGINE_TMA_BULK, STRATA_ENGINE_DMA,
                    STRATA_H2D, STRATA_HOST_HUGEPAGES, STRATA_HOST_NO_NUMA_BIND, STRATA_POOL_SINGLE_KV,
                    STRATA_HOST_HEAD_MAJOR,
-                   STRATA_HOST_WRITECOMBINED, STRATA_VALIDATE, PoolDesc, StrataError, Xfer, check)
+                   STRATA_HOST_WRITECOMBINED, STRATA_VALIDATE, STRATA_ERR_UNSUPPORTED, PoolDesc, StrataError,
+                   Xfer, check)
 
 __all__ = [
     "strata_register_host_pool", "strata_unregister_host_pool", "strata_host_pool_ptr", "strata_load",
     "strata_offload", "strata_layer_event", "strata_wait_layer", "strata_layer_elapsed_ms",
-    "strata_baseline_memcpy_pages", "strata_baseline_contiguous",
+    "strata_baseline_memcpy_pages", "strata_baseline_contiguous", "strata_test_ring_geometry",
     "strata_version", "strata_get_counters", "HostPool", "Requests", "StrataError",
 ]
 
@@ -112,6 +113,19 @@ def strata_baseline_memcpy_pages(pool: int, xfer: Xfer, direction: int, stream=N
                                                   ctypes.c_void_p(_stream_handle(stream)), ctypes.byref(n)),
           "strata_baseline_memcpy_pages")
     return int(n.value)
+
+
+def strata_test_ring_geometry(tok_bytes: int, chunk_tokens: int, gran: int, smem_budget: int, inflight_bytes: int,
+                              ctas: int, warps: int, stage_target: int):
+    """The ring engine's per-CTA geometry (include/strata_test.h): (rows per piece, stages, warps,
+    stage bytes), or None when no 2-stage ring fits."""
+    out = (ctypes.c_int32 * 4)()
+    rc = _lib.lib().strata_test_ring_geometry(tok_bytes, chunk_tokens, gran, smem_budget, inflight_bytes, ctas, warps,
+                                              stage_target, out)
+    if rc == STRATA_ERR_UNSUPPORTED:
+        return None
+    check(rc, "strata_test_ring_geometry")
+    return tuple(out)
 
 
 def strata_baseline_contiguous(pool: int, direction: int, dev_ptr: int, host_offset: int, nbytes: int,

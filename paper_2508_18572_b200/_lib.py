@@ -111,6 +111,9 @@ _SIGS = {
                                                     ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "strata_baseline_contiguous": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
                                                   ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
+    "strata_test_ring_geometry": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.POINTER(ctypes.c_int32)]),
 }
 
 

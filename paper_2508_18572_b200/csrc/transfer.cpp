@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "../../include/strata_test.h"
 
 namespace strata {
 
@@ -294,38 +295,28 @@ static bool ring_supported(const strata_pool* p, int dir) {
          reinterpret_cast<uintptr_t>(p->host_dev) % 16 == 0 && p->host_bytes % 16 == 0;
 }
 
-// Ring geometry for this pool and direction (rows per piece, stages, scatter warps); false when a
-// 2-stage ring of one-row pieces does not fit in shared memory.
-static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const XferParams& xp, int ctas,
-                      RingParams& rp) {
-  const int tok = static_cast<int>(p->tok_bytes);
-  int W = x->threads ? x->threads / 32 - 1
-                     : dir == 0 ? env_int("STRATA_RING_WARPS", kDefaultRingWarps)
-                                : env_int("STRATA_RING_GATHER_WARPS", kDefaultRingGatherWarps);
+// The ring's per-CTA geometry, a pure function of sizes (exported for tests: strata_test_ring_geometry).
+// R rows per piece (a piece = one host run, <= stage_target bytes, <= C tokens, <= kRingMaxRows);
+// S stages holding inflight / ctas host bytes (2..kRingMaxStages, within the shared-memory budget);
+// W device-side warps, a divisor of S (stage s belongs to warp s % W, ring.cu).
+struct RingGeom {
+  int R = 0, S = 0, W = 0, sb = 0;
+};
+static bool ring_geometry(int tok, int C, int gran, int budget, int64_t inflight, int ctas, int W, int target,
+                          RingGeom& g) {
   W = std::max(1, std::min(kRingMaxWarps, W));
-  const int target = std::max(1, env_int("STRATA_RING_STAGE_KB", kDefaultRingStageKB)) << 10;
-  int R = std::min<int>(p->d.chunk_tokens, std::max(1, target / tok));
+  int R = std::min<int>(C, std::max(1, target / tok));
   R = std::min(R, kRingMaxRows);
   // narrow rows: the stage holds the run's enclosing 16-byte-aligned span (up to 30 bytes more)
-  const int sb = (R * tok + (p->gran < 16 ? 32 : 0) + 127) / 128 * 128;
-  int budget = p->tma_smem;
-  const int cap_kb = env_int("STRATA_RING_SMEM_KB", 0);
-  if (cap_kb > 0) budget = std::min(budget, cap_kb << 10);
-  // host bytes kept in flight (the rings' capacity) over all CTAs: the caller's bound
-  // (strata_xfer.inflight_kib), else the default — the knee of the throughput / interference
-  // frontier (DESIGN.md §6): more than the link needs only queues requests, and queued host reads
-  // are what slows co-running HBM-bound work
-  const int64_t total = x->inflight_kib > 0 ? x->inflight_kib
-                        : env_int("STRATA_RING_INFLIGHT_KB", tok < kRingShortRowBytes ? kDefaultRingInflightShortKB
-                                                                                     : kDefaultRingInflightKB);
-  const int64_t per_cta = (total << 10) / std::max(1, ctas);
+  const int sb = (R * tok + (gran < 16 ? 32 : 0) + 127) / 128 * 128;
+  const int64_t per_cta = inflight / std::max(1, ctas);
   int S = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(kRingMaxStages, per_cta / sb)));
   S = std::min(S, env_int("STRATA_RING_STAGES", kRingMaxStages));
   while (S >= 2 && ring_header_bytes() + S * sb > budget) --S;
   if (S < 2) return false;
-  // stage s belongs to device-side warp s % W (ring.cu), so W must divide S: take the largest S' <= S
-  // with a divisor d <= W of at least half of min(W, S') and run d warps (S = 13, W = 8 would otherwise
-  // leave ONE scatter warp: 16.4 GB/s instead of 51, profiles/r02/sweep70/)
+  // W must divide S: take the largest S' <= S with a divisor d <= W of at least half of min(W, S')
+  // and run d warps (S = 13, W = 8 would otherwise leave ONE scatter warp: 16.4 GB/s instead of 51,
+  // profiles/r02/sweep70/)
   int Wd = 1;
   for (int s2 = S; s2 >= 2; --s2) {
     int d = 1;
@@ -337,14 +328,42 @@ static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const
       break;
     }
   }
-  W = Wd;
+  g.R = R;
+  g.S = S;
+  g.W = Wd;
+  g.sb = sb;
+  return true;
+}
+
+// Ring geometry for this pool and direction (rows per piece, stages, scatter warps); false when a
+// 2-stage ring of one-row pieces does not fit in shared memory.
+static bool plan_ring(const strata_pool* p, const strata_xfer* x, int dir, const XferParams& xp, int ctas,
+                      RingParams& rp) {
+  const int tok = static_cast<int>(p->tok_bytes);
+  const int W = x->threads ? x->threads / 32 - 1
+                           : dir == 0 ? env_int("STRATA_RING_WARPS", kDefaultRingWarps)
+                                      : env_int("STRATA_RING_GATHER_WARPS", kDefaultRingGatherWarps);
+  const int target = std::max(1, env_int("STRATA_RING_STAGE_KB", kDefaultRingStageKB)) << 10;
+  int budget = p->tma_smem;
+  const int cap_kb = env_int("STRATA_RING_SMEM_KB", 0);
+  if (cap_kb > 0) budget = std::min(budget, cap_kb << 10);
+  // host bytes kept in flight (the rings' capacity) over all CTAs: the caller's bound
+  // (strata_xfer.inflight_kib), else the default — the knee of the throughput / interference
+  // frontier (DESIGN.md §6): more than the link needs only queues requests, and queued host reads
+  // are what slows co-running HBM-bound work
+  const int64_t total = x->inflight_kib > 0 ? x->inflight_kib
+                        : env_int("STRATA_RING_INFLIGHT_KB", tok < kRingShortRowBytes ? kDefaultRingInflightShortKB
+                                                                                     : kDefaultRingInflightKB);
+  RingGeom geo;
+  if (!ring_geometry(tok, p->d.chunk_tokens, p->gran, budget, total << 10, ctas, W, target, geo)) return false;
+  const int R = geo.R, S = geo.S, sb = geo.sb;
   std::memset(&rp, 0, offsetof(RingParams, pair_end));
   rp.x = xp;
   rp.rows = R;
   rp.stages = S;
   rp.stage_bytes = sb;
   rp.pps = (p->d.chunk_tokens + R - 1) / R;
-  rp.warps = W;
+  rp.warps = geo.W;
   rp.host_run = p->host_tok_stride == p->tok_bytes;
   rp.bulk_store = dir == 0 && env_int("STRATA_RING_BULK_STORE", 0) != 0;
   rp.debug = env_int("STRATA_RING_DEBUG", 0);
@@ -701,3 +720,19 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
 
 
 }  // namespace strata
+
+extern "C" int strata_test_ring_geometry(int32_t tok_bytes, int32_t chunk_tokens, int32_t gran, int32_t smem_budget,
+                                         int64_t inflight_bytes, int32_t ctas, int32_t warps, int32_t stage_target,
+                                         int32_t out[4]) {
+  if (!out || tok_bytes <= 0 || chunk_tokens <= 0 || gran <= 0 || smem_budget <= 0 || inflight_bytes <= 0 ||
+      ctas <= 0 || warps <= 0 || stage_target <= 0)
+    return STRATA_ERR_INVALID_ARG;
+  strata::RingGeom g;
+  if (!strata::ring_geometry(tok_bytes, chunk_tokens, gran, smem_budget, inflight_bytes, ctas, warps, stage_target, g))
+    return STRATA_ERR_UNSUPPORTED;
+  out[0] = g.R;
+  out[1] = g.S;
+  out[2] = g.W;
+  out[3] = g.sb;
+  return STRATA_OK;
+}
