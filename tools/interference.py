@@ -75,6 +75,61 @@ def make_decode():
     return run
 
 
+def _attn_layers(batch=16, ctx=4096, page=16, layers=32):
+    """The paper's decode pass (16 requests x 4K) with the real kernel: FlashInfer paged
+    decode attention, Llama-3.1-8B heads (32 query / 8 KV heads, d = 128, bf16), page size 16, one
+    KV cache per layer (256 MiB each at the defaults), the pages of every request scattered."""
+    import flashinfer
+    npg = batch * ctx // page
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    caches = [(torch.randn(npg, page, 8, 128, dtype=torch.bfloat16, device="cuda", generator=gen),
+               torch.randn(npg, page, 8, 128, dtype=torch.bfloat16, device="cuda", generator=gen))
+              for _ in range(layers)]
+    ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    w = flashinfer.BatchDecodeWithPagedKVCacheWrapper(ws, "NHD")
+    indices = torch.randperm(npg, device="cuda", generator=gen).to(torch.int32)
+    indptr = torch.arange(0, npg + 1, ctx // page, dtype=torch.int32, device="cuda")
+    last = torch.full((batch,), page, dtype=torch.int32, device="cuda")
+    w.plan(indptr, indices, last, 32, 8, 128, page, q_data_type=torch.bfloat16, kv_data_type=torch.bfloat16)
+    q = torch.randn(batch, 32, 128, dtype=torch.bfloat16, device="cuda", generator=gen)
+    out = torch.empty_like(q)
+    return w, q, out, caches
+
+
+def make_attn():
+    w, q, out, caches = _attn_layers()
+
+    def run():
+        for c in caches:
+            w.run(q, c, out=out)
+    return run
+
+
+def make_decode_step():
+    """A whole Llama-3.1-8B decode step at batch 16 x 4K context, every layer's kernels in order:
+    RMSNorm, QKV GEMM, FlashInfer paged decode attention, O GEMM, RMSNorm, gate/up GEMM, SiLU x up,
+    down GEMM (random bf16 weights, 14 GiB; KV as in make_attn)."""
+    w, q, out, caches = _attn_layers()
+    B, Hd = 16, 4096
+    gen = torch.Generator(device="cuda").manual_seed(8)
+    mk = lambda *s: torch.randn(*s, dtype=torch.bfloat16, device="cuda", generator=gen) * 0.02  # noqa: E731
+    layers = [(mk(Hd, 6144), mk(Hd, Hd), mk(Hd, 2 * 14336), mk(14336, Hd), mk(Hd), mk(Hd)) for _ in caches]
+    x = torch.randn(B, Hd, dtype=torch.bfloat16, device="cuda", generator=gen)
+
+    def run():
+        h = x
+        for (wqkv, wo, wgu, wd, n1, n2), c in zip(layers, caches):
+            a = torch.nn.functional.rms_norm(h, (Hd,), n1)
+            qkv = a @ wqkv
+            w.run(qkv[:, :Hd].reshape(B, 32, 128), c, out=out)
+            h = h + out.reshape(B, Hd) @ wo
+            a = torch.nn.functional.rms_norm(h, (Hd,), n2)
+            gu = a @ wgu
+            h = h + (torch.nn.functional.silu(gu[:, :14336]) * gu[:, 14336:]) @ wd
+        return h
+    return run
+
+
 CLOCKS = []   # (sm MHz, power W) samples of the last time_proxy block
 
 
@@ -139,7 +194,7 @@ def main():
     ap.add_argument("--P", type=int, default=1, help="device page size")
     ap.add_argument("--flags", type=int, default=0, help="strata_pool_desc.flags of the host tier (1 = huge pages)")
     ap.add_argument("--tag", default="")
-    ap.add_argument("--proxies", default="prefill,decode", help="prefill, decode, decode1 (one-kernel decode)")
+    ap.add_argument("--proxies", default="prefill,decode", help="prefill, decode, decode1 (one-kernel decode), decodeN (N kernels), attn (FlashInfer decode attention), decode_step (a whole Llama-8B decode step)")
     ap.add_argument("--offload", type=int, default=0, help="1: co-run offloads (write-back) instead of loads")
     args = ap.parse_args()
 
@@ -155,7 +210,8 @@ def main():
     lo, hi = torch.cuda.Stream.priority_range()
     io = torch.cuda.Stream(priority=hi)       # I/O: high priority (its few CTAs get SMs first)
     comp = torch.cuda.Stream(priority=lo)
-    makers = {"prefill": make_prefill, "decode": make_decode, "decode1": make_decode1}
+    makers = {"prefill": make_prefill, "decode": make_decode, "decode1": make_decode1, "attn": make_attn,
+              "decode_step": make_decode_step}
     # decodeN: the same 8 GiB HBM read split into N reduction kernels (per-kernel-boundary cost)
     proxies = {name: (makers[name]() if name in makers else make_decode_split(int(name[len("decode"):])))
                for name in args.proxies.split(",")}
