@@ -234,7 +234,8 @@ def interference(torch, pool, reqs, io, bytes_load, link):
     slowed by this workload's default load.  One alone / beside pair per proxy after a 0.5 s idle,
     10 timed repetitions each (tests/test_gpu_interference.py runs the full 3-round protocol):
     prefill = bf16 GEMMs of a Llama-8B layer for 2 x 4K tokens; decode = an 8 GiB HBM read of 16 x 4K
-    tokens of KV for 32 layers as 32 kernels; decode_long = the same read as 4 kernels."""
+    tokens of KV for 32 layers as 32 kernels; decode_long = the same read as 4 kernels; attn = the same
+    KV as the paper's decode pass run by a real kernel (FlashInfer paged decode attention, 32 layers)."""
     lo, hi = torch.cuda.Stream.priority_range()
     comp = torch.cuda.Stream(priority=lo)
     M = 8192
@@ -246,6 +247,26 @@ def interference(torch, pool, reqs, io, bytes_load, link):
     proxies = {"prefill": lambda: [torch.matmul(xs[k], w) for (k, _), w in zip(shapes, ws)],
                "decode": lambda: [t.sum(dtype=torch.float32) for t in parts32],
                "decode_long": lambda: [t.sum(dtype=torch.float32) for t in parts4]}
+    attn_note = None
+    try:
+        # the paper's decode pass with a real decode kernel: FlashInfer paged decode attention, 16
+        # requests x 4K tokens, Llama-8B heads, page 16, scattered pages, one kernel per layer x 32
+        import flashinfer
+        npg = 16 * 4096 // 16
+        gen = torch.Generator(device="cuda").manual_seed(7)
+        # the 8 GiB KV of the read proxies, viewed as 32 paged K/V caches of 256 MiB each
+        caches = [tuple(t.view(2, npg, 16, 8, 128)) for t in parts32]
+        wr = flashinfer.BatchDecodeWithPagedKVCacheWrapper(torch.empty(256 << 20, dtype=torch.uint8, device="cuda"),
+                                                           "NHD")
+        wr.plan(torch.arange(0, npg + 1, 4096 // 16, dtype=torch.int32, device="cuda"),
+                torch.randperm(npg, device="cuda", generator=gen).to(torch.int32),
+                torch.full((16,), 16, dtype=torch.int32, device="cuda"), 32, 8, 128, 16,
+                q_data_type=torch.bfloat16, kv_data_type=torch.bfloat16)
+        qd = torch.randn(16, 32, 128, dtype=torch.bfloat16, device="cuda", generator=gen)
+        od = torch.empty_like(qd)
+        proxies["attn"] = lambda: [wr.run(qd, c, out=od) for c in caches]
+    except Exception as ex:   # FlashInfer missing or failing on this box: the other proxies still run
+        attn_note = f"attn proxy unavailable: {type(ex).__name__}: {str(ex)[:120]}"
 
     def run(fn, reps=10):
         evs = []
@@ -278,8 +299,10 @@ def interference(torch, pool, reqs, io, bytes_load, link):
         rates.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
         out[name] = round(co / alone - 1, 4)
     out["load_gbs_beside"] = round(statistics.median(rates), 3)
+    if attn_note:
+        out["attn_note"] = attn_note
     out["paper_budget"] = {"prefill": 0.05, "decode": 0.10, "source": "PAPER.md:262 (H200, ~50 GB/s)"}
-    del xs, ws, kv, parts32, parts4
+    del xs, ws, kv, parts32, parts4, proxies
     torch.cuda.empty_cache()
     return out
 

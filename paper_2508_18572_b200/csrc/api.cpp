@@ -400,6 +400,7 @@ int strata_register_host_pool(const strata_pool_desc* d, strata_pool_t* out) {
   }
   for (auto& op : p->ops) op = {0, 0, 0};
   p->tma_smem = strata::tma_smem_limit();
+  p->loads_active = strata::ring_loads_active();   // resolved here, never under stream capture
   if (p->tma_smem > 0 && ((e = strata::tma_prepare(p->tma_smem)) || (e = strata::ring_prepare(p->tma_smem)))) {
     destroy(p);
     return cuda_fail(e, "cudaFuncSetAttribute(TMA smem)");

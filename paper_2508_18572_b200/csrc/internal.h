@@ -90,6 +90,8 @@ struct FusedParams {
   int32_t total_warps;          // warps in the grid (each arrives once per layer)
   uint32_t* counters;           // [L] arrival counters of this op slot (0 on entry, reset by the kernel)
   uint32_t* flags;              // [L] completion flags of this op slot
+  uint32_t* loads_active;       // load: the device-wide running-load counter ring offloads pace beside
+                                // (ring_loads_active()); NULL for offloads
   char* kb[kMaxFusedLayers];    // per-layer K / V bases
   char* vb[kMaxFusedLayers];
 };
@@ -130,6 +132,10 @@ struct RingParams {
 };
 // Shared-memory bytes in front of the ring's stages (mbarriers).
 int ring_header_bytes();
+// Device address of the running-load counter of the current device (ring.cu's g_loads_active): every
+// running load CTA (ring, fused LDG) counts itself in it; ring offloads pace their host stores while
+// it is non-zero.
+uint32_t* ring_loads_active();
 cudaError_t launch_ring(const RingParams& p, int dir, int ctas, cudaStream_t s);
 cudaError_t ring_prepare(int smem);
 
@@ -190,6 +196,7 @@ struct strata_pool {
   int32_t* err_dev = nullptr;
   int32_t* err_host = nullptr;        // pinned
   int tma_smem = 0;
+  uint32_t* loads_active = nullptr;   // device address of the running-load counter (ring_loads_active())
   strata_counters counters = {};
   // STRATA_ENGINE_DMA, one state per direction (0 load, 1 offload; lazy): a double-buffered HBM
   // staging ring, copy streams and their events.  Separate per direction so a load and an offload

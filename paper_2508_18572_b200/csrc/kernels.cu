@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const RowIdx first = ldg_first(p, warp, lane);
   const int64_t layer_step = static_cast<int64_t>(p.nkv) * p.kv_off;
+  if (DIR == 0 && fp.loads_active && threadIdx.x == 0) atomicAdd(fp.loads_active, 1u);   // ring offloads yield
   for (int l = fp.l0; l < fp.l1; ++l) {
     ldg_layer<U, CONTIG, HCONTIG, DIR>(p, fp.kb[l], fp.vb[l], int64_t(l) * layer_step, first, warp, nwarps, lane);
     __syncwarp();
@@ -205,6 +206,10 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const
         st_release<DIR>(fp.flags + l, fp.epoch);
       }
     }
+  }
+  if (DIR == 0 && fp.loads_active) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicSub(fp.loads_active, 1u);
   }
 }
 

@@ -37,8 +37,8 @@ using namespace dev;
 constexpr int kRingBarBytes = 2 * kRingMaxStages * 8 + kRingMaxStages * 4;   // full[16], empty[16], pad[16]
 constexpr int kU = 4;                                   // 16-byte vectors in flight per scatter lane
 
-// Ring-load CTAs running on this device (all pools of the process): offloads yield the host link to
-// loads while it is non-zero (RingParams::yield_k).
+// Load CTAs running on this device (ring loads and fused LDG loads of all pools of the process): ring
+// offloads pace their host stores while it is non-zero (RingParams::pace_ps_per_byte).
 __device__ unsigned int g_loads_active;
 
 // [full[16] | empty[16] | pad[16] (narrow rows: host-run offset in its 16-byte unit) | pad to 128 | S stages]
@@ -537,6 +537,15 @@ __global__ void __launch_bounds__(32 * (1 + kRingMaxWarps), 1) ring_offload_kern
 }  // namespace
 
 int ring_header_bytes() { return ring_buf_offset(); }
+
+uint32_t* ring_loads_active() {
+  void* a = nullptr;
+  if (cudaGetSymbolAddress(&a, g_loads_active) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;   // the LDG load then runs uncounted (offloads beside it unpaced)
+  }
+  return static_cast<uint32_t*>(a);
+}
 
 cudaError_t launch_ring(const RingParams& p, int dir, int ctas, cudaStream_t s) {
   // exclusive: reserve the SM's shared memory so no other kernel's CTA shares the SM

@@ -675,6 +675,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     fp.total_warps = fctas * threads / 32;
     fp.counters = counters;
     fp.flags = counters + L;
+    fp.loads_active = dir == 0 ? p->loads_active : nullptr;
     for (int l = 0; l < L; ++l) {
       fp.kb[l] = static_cast<char*>(p->k[l]);
       fp.vb[l] = static_cast<char*>(p->v[l]);

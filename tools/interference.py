@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--ring-stage", default="0", help="ring engine piece sizes in KiB (0 = default; STRATA_RING_STAGE_KB)")
     ap.add_argument("--ring-configs", default="",
                     help="explicit ring geometries 'ctas:stage_kb:smem_kb:warps,...' (replaces the engine x ctas grid)")
+    ap.add_argument("--env-sets", default="",
+                    help="ring loads (engine 2, default quota) under explicit library environments: "
+                         "'K=V;K=V,K=V,...' (e.g. STRATA_RING_LOAD_PACE_MBS=48000;STRATA_RING_INFLIGHT_KB=320)")
     ap.add_argument("--memcpy", type=int, default=0, help="also co-run a contiguous cudaMemcpyAsync loop (-1 engine)")
     ap.add_argument("--cooldown", type=float, default=1.0,
                     help="idle seconds before every alone / co-run block (power-state reset for the GEMM proxy)")
@@ -233,7 +236,7 @@ def main():
 
     def make_io(eng, c, G, env):
         for key in ("STRATA_RING_SMEM_KB", "STRATA_RING_STAGE_KB", "STRATA_RING_WARPS", "STRATA_RING_DEBUG",
-                    "STRATA_RING_EXCLUSIVE"):
+                    "STRATA_RING_EXCLUSIVE", "STRATA_RING_LOAD_PACE_MBS", "STRATA_RING_INFLIGHT_KB"):
             os.environ.pop(key, None)
         os.environ.update(env)
         if eng < 0:   # contiguous memcpy of the same bytes: 32 copies of one layer's worth
@@ -266,6 +269,9 @@ def main():
             if len(f) > 5:   # optional 6th field: STRATA_RING_DEBUG bits (A/B only)
                 env["STRATA_RING_DEBUG"] = f[5]
             configs.append((2, c, 0, env))
+    if args.env_sets:
+        configs = [(2, 0, 0, dict(kv.split("=", 1) for kv in item.split(";") if kv))
+                   for item in args.env_sets.split(",")]
     if args.memcpy:
         configs.append((-1, 0, 0, {}))
     for eng, c, G, env in configs:
