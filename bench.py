@@ -5,8 +5,10 @@ One "step" = one strata_load of the whole cached prefix, every layer (all §8(a)
 index fetch + layout transform, host->HBM movement, per-layer completion flags/events) — for the
 default workload BASELINE.json configs[1]: Llama-3.1-8B geometry (32 layers, 8 KV heads, d=128,
 bf16), a 32K-token prefix, page size 1, randomly fragmented pages, 4 GiB per step (> 126 MB L2, so no
-flush is needed).  The default engine is the hand-written zero-copy ring kernel (csrc/ring.cu):
-TMA bulk reads of the page-first host runs through the tier's UVA mapping, LSU scatter to the pages.
+flush is needed).  The default engine for such a load is the hand-written zero-copy LDG kernel
+(csrc/kernels.cu, the paper's 2 x 1024-thread configuration): 16-byte loads of the page-first host
+rows through the tier's UVA mapping, register-staged stores to the pages.  The TMA-fed ring kernel
+(csrc/ring.cu) is reported beside it under other_engines_gbs.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl strata|reference] [--config ...] [--page-size P]
 
@@ -42,7 +44,11 @@ PATH_DESC = {
             "(one cp.async.bulk per page-first host run of <= 16 KiB, from the UVA-mapped tier, into a 7-stage "
             "shared-memory ring) + up to 8 LSU scatter warps (16-byte st.global to the pages); per-layer completion "
             "flags -> layer events",
-    "ldg": "ldg_fused_kernel (csrc/kernels.cu): zero-copy 16-byte LDG/STG register staging, one launch for all layers",
+    "ldg": "ldg_fused_kernel (csrc/kernels.cu): ONE launch for all layers, 2 CTAs x 1024 threads (the paper's "
+           "configuration, PAPER.md:262); a warp owns 32 rows, lane t fetches row t's chunk / page indices one group "
+           "ahead and the addresses go out by __shfl_sync, each lane keeps 4 independent 16-byte "
+           "ld.global.nc.L1::no_allocate.v4 reads of the UVA-mapped tier in flight, then st.global.v4 to the pages; "
+           "per-layer completion flags -> layer events",
     "dma": "per layer: copy-engine gather of the page-first chunk-layer runs (one cudaMemcpyAsync per run) into an HBM "
            "staging slot + ldg_kernel scatter to the pages",
     "tma_bulk": "tma_kernel (csrc/kernels.cu): one warp per CTA, cp.async.bulk on both sides of a smem ring",
@@ -59,7 +65,7 @@ def parse(argv=None):
     ap.add_argument("--page-size", type=int, default=None)
     ap.add_argument("--chunk-tokens", type=int, default=None,
                     help="host chunk size C (the host tier keeps the same token capacity)")
-    ap.add_argument("--engine", type=int, default=0, help="0 default (ring), 1 LDG, 2 ring, 3 TMA bulk, 4 DMA")
+    ap.add_argument("--engine", type=int, default=0, help="0 default (LDG for loads >= 16 MiB of 16-byte rows, else ring), 1 LDG, 2 ring, 3 TMA bulk, 4 DMA")
     ap.add_argument("--num-ctas", type=int, default=0)
     ap.add_argument("--layer-group", type=int, default=0, help="DMA engine: layers per copy run (0 = library default)")
     ap.add_argument("--frag", default="perm", choices=["perm", "churn"])

@@ -121,11 +121,15 @@ enum strata_pool_flags {
 
 /* Transfer engines (strata_xfer.engine). Both are bit-identical; they differ in how bytes move. */
 enum strata_engine {
-  STRATA_ENGINE_DEFAULT = 0,  /* library choice: a zero-copy kernel — STRATA_ENGINE_TMA (the ring)
-                                 wherever the tier has whole host rows in 16-byte units (and for
+  STRATA_ENGINE_DEFAULT = 0,  /* library choice, always a zero-copy kernel: loads of >= 16 MiB of
+                                 16-byte-granular rows take STRATA_ENGINE_LDG at the paper's 2 x 1024
+                                 threads (the same ~51 GB/s as the ring, less interference with
+                                 co-running decode: DESIGN.md §6.1); otherwise STRATA_ENGINE_TMA (the
+                                 ring) wherever the tier has whole host rows in 16-byte units (and for
                                  loads of 8- / 4-byte-granular narrow rows), else STRATA_ENGINE_LDG.
                                  The copy engines (DMA) run only when asked for. */
-  STRATA_ENGINE_LDG = 1,      /* warps, 16-byte LDG/STG register staging, warp index broadcast */
+  STRATA_ENGINE_LDG = 1,      /* warps, 16-byte LDG/STG register staging, warp index broadcast; >= 2
+                                 CTAs run every layer in one launch */
   STRATA_ENGINE_TMA = 2,      /* the ring engine: one persistent launch per operation; per CTA a TMA
                                  warp moves each page-first host run (<= 16 KiB piece) with one
                                  cp.async.bulk through a shared-memory ring, LSU warps scatter the

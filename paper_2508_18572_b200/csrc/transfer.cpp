@@ -505,11 +505,20 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   xp.wph_magic = (xp.wph & (xp.wph - 1)) ? div_magic(xp.wph, xp.wpr) : 0;
 
   // Engine.  The default is a hand-written zero-copy kernel reading / writing the host tier through
-  // its UVA mapping: the ring engine where the tier has whole host rows in 16-byte
-  // units, else the LDG engine (narrow rows R29, head-major tiers with several heads per GPU).  The
-  // copy-engine path (STRATA_ENGINE_DMA) runs only when a caller asks for it.
+  // its UVA mapping.  Loads of 16-byte-granular rows of >= kSmallOpBytes take the LDG
+  // engine at the paper's configuration (2 CTAs x 1024 threads, one fused launch): it moves
+  // the ring's ~51 GB/s on Llama-8B and slows co-running decode attention less (+7 vs +9 %, DESIGN.md
+  // §6.1, NEXT-1).  Everything else — offloads, small (latency-bound) loads, narrow rows of 8- / 4-byte
+  // granularity — takes the ring engine where the tier has whole host rows in 16-byte units, else
+  // LDG (narrow offloads, head-major tiers with several heads per GPU).  The copy-engine path
+  // (STRATA_ENGINE_DMA) runs only when a caller asks for it.
   int engine = x->engine;
-  if (engine == STRATA_ENGINE_DEFAULT) engine = ring_supported(p, dir) ? STRATA_ENGINE_TMA : STRATA_ENGINE_LDG;
+  if (engine == STRATA_ENGINE_DEFAULT) {
+    const int64_t op_bytes = int64_t(p->nkv) * plan.total_tokens * p->tok_bytes * (x->layer_end - x->layer_begin);
+    engine = dir == 0 && p->gran == 16 && op_bytes >= kSmallOpBytes ? STRATA_ENGINE_LDG
+             : ring_supported(p, dir)                                 ? STRATA_ENGINE_TMA
+                                                                      : STRATA_ENGINE_LDG;
+  }
   // the copy engines need long host runs: a token-major tier read in a head slice (Ht > H) has
   // only H*D*e bytes per token contiguous, so its DMA requests run on the LDG engine instead
   if (engine == STRATA_ENGINE_DMA && !dma_runs_ok(p)) engine = STRATA_ENGINE_LDG;

@@ -11,9 +11,10 @@ import oracle
 from tests.helpers import CANARY
 
 
-def default_engine(g, strides=None, direction: str = "load") -> int:
-    """The engine strata_load/offload pick with STRATA_ENGINE_DEFAULT (transfer.cpp ring_supported):
-    the ring engine (STRATA_ENGINE_TMA) when the tier has whole host rows in 16-byte units — or, for
+def default_engine(g, strides=None, direction: str = "load", op_bytes: int = 0) -> int:
+    """The engine strata_load/offload pick with STRATA_ENGINE_DEFAULT (transfer.cpp): loads of
+    16-byte-granular rows of >= 16 MiB take the LDG engine (the paper's configuration, NEXT-1);
+    otherwise the ring engine (STRATA_ENGINE_TMA) when the tier has whole host rows in 16-byte units — or, for
     loads, narrow rows (R29) of 8- or 4-byte granularity whose host rows of a chunk form one run and
     whose device rows are head-contiguous; else LDG (a head-major tier with several heads per GPU,
     narrow offloads, 2- / 1-byte granularity).  Assumes a library-allocated (aligned) host tier."""
@@ -25,6 +26,8 @@ def default_engine(g, strides=None, direction: str = "load") -> int:
     for v in vals:
         while gran > 1 and v % gran:
             gran //= 2
+    if gran == 16 and direction == "load" and op_bytes >= 16 << 20:
+        return st.STRATA_ENGINE_LDG
     if gran == 16:
         return st.STRATA_ENGINE_TMA
     Ht = getattr(g, "Ht", 0) or g.H

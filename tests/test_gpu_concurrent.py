@@ -74,14 +74,14 @@ def test_two_operations_in_flight(kinds, ea, eb):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("load_engine", [st.STRATA_ENGINE_DEFAULT, LDG])
+@pytest.mark.parametrize("load_engine", [TMA, LDG])
 def test_load_keeps_the_link_beside_a_running_offload(load_engine):
     """A load and an offload of one pool in flight together (a serving engine loads the next batch's
     prefixes while it backs up finished ones): the offload paces itself while the load
     runs (the backup is the non-critical path), so the load keeps >= 85 % of its
     solo rate; both results stay bit-exact.  Without pacing the load fell to ~15 GB/s
-    (profiles/r02/bidir/).  Both zero-copy load engines (the ring default and the fused LDG kernel)
-    count themselves in the device-wide running-load counter the offload paces against."""
+    (profiles/r02/bidir/).  Both zero-copy load engines (the ring and the fused LDG kernel, the
+    default for large loads) count themselves in the device-wide running-load counter the offload paces against."""
     L, n = 16, 32768
     g = Geometry(L, 8, 128, 2, 1, 64, 2 * 41000, 2 * 520)
     rng = kvgen.rng_for(41)

@@ -129,8 +129,12 @@ def test_llama70b_tp8_shared_tier_bench_config():
     try:
         c.pool.load(c.reqs)
         torch.cuda.synchronize()
-        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_TMA
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_LDG   # default for >= 16 MiB loads
         c.check_load(0, g.L, layers=[0, 41, 79])
+        c.pool.load(c.reqs, engine=st.STRATA_ENGINE_TMA)
+        torch.cuda.synchronize()
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_TMA
+        c.check_load(0, g.L, layers=[5, 79])
     finally:
         c.close()
 

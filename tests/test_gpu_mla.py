@@ -110,7 +110,7 @@ def test_deepseek_v3_mla_32k_full():
     try:
         t = c.pool.load(c.reqs)
         torch.cuda.synchronize()
-        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_TMA
+        assert c.pool.counters()["last_engine"] == st.STRATA_ENGINE_LDG   # default for >= 16 MiB loads
         for l in (0, 1, 30, 60):
             assert c.pool.layer_elapsed_ms(t, l) > 0
         c.check_load(0, g.L, layers=[0, 1, 30, 59, 60])

@@ -456,10 +456,11 @@ def test_caller_owned_host_memory():
 # Full-size configs (BASELINE.json), in the launch configuration bench.py times.
 @pytest.mark.slow
 @pytest.mark.parametrize("P,engine", [(1, st.STRATA_ENGINE_DEFAULT), (16, st.STRATA_ENGINE_DEFAULT),
-                                      (1, st.STRATA_ENGINE_LDG)])
+                                      (1, st.STRATA_ENGINE_TMA), (16, st.STRATA_ENGINE_TMA)])
 def test_llama8b_32k_full(P, engine):
     """Every byte of all 32 layers, in bench.py's launch configuration (default engine and quota:
-    the zero-copy ring engine) and with the zero-copy LDG engine at its default 2-CTA quota."""
+    the zero-copy LDG engine, 2 CTAs x 1024 threads, one fused launch) and with the zero-copy ring
+    engine at its default 2-CTA quota."""
     g = kvgen.geometry("llama8b_32k", P=P)
     q = kvgen.make_requests(kvgen.rng_for(0), [32768], g.P, g.C, g.num_pages, g.num_chunks)
     c = GpuCase(g, q)
@@ -468,7 +469,7 @@ def test_llama8b_32k_full(P, engine):
         _sync()
         c.check_load(0, g.L)
         used = c.pool.counters()["last_engine"]
-        assert used == (st.STRATA_ENGINE_TMA if engine == st.STRATA_ENGINE_DEFAULT else engine)
+        assert used == (st.STRATA_ENGINE_LDG if engine == st.STRATA_ENGINE_DEFAULT else engine)
     finally:
         c.close()
 

@@ -37,7 +37,7 @@ def _bf16_host(pool, g, seed):
 
 
 @pytest.mark.parametrize("engine,P", [(st.STRATA_ENGINE_DEFAULT, 1), (st.STRATA_ENGINE_DEFAULT, 16),
-                                      (st.STRATA_ENGINE_LDG, 1)])
+                                      (st.STRATA_ENGINE_TMA, 1)])
 def test_layerwise_prefill_over_streaming_pages_matches_oracle_kv(engine, P):
     flashinfer = pytest.importorskip("flashinfer")
     cached, new = 16384, 256
