@@ -250,6 +250,20 @@ int strata_offload(strata_pool_t p, const strata_xfer* x, strata_stream_t stream
  * layer flags it shares), so a layer event never fires before that layer's bytes landed. */
 int strata_layer_event(strata_pool_t p, uint64_t ticket, int32_t layer, strata_event_t* out);
 
+/* Decode-aware SM quota (NEXT-1; "a small number of large CUDA blocks", DESIGN.md
+ * §6.1): a stream-ordered cap on the CTAs that take new work in this pool's running and later
+ * one-launch LDG loads (the default engine for loads >= 16 MiB of 16-byte rows).  Enqueues on
+ * `stream` a device write of `max_ctas` to the pool's quota word (cuStreamWriteValue32); 0 lifts
+ * the cap.  Loads launched after the FIRST call assign row groups dynamically: while the cap is
+ * q > 0, CTAs q, q+1, ... take no new rows (their SMs keep no host reads in flight) and CTAs
+ * 0..q-1 move the rest, so every result stays bit-exact and every layer event still fires.  Typical
+ * use: strata_set_load_quota(pool, 1, decode_stream) before a decode step, (pool, 0, decode_stream)
+ * after it.  Loads launched before the first call, ring / per-layer launches and offloads ignore
+ * it.  The first call allocates the word and must not run under stream capture
+ * (STRATA_ERR_UNSUPPORTED); later calls may be captured.  Errors: STRATA_ERR_INVALID_ARG
+ * (max_ctas < 0), STRATA_ERR_UNSUPPORTED (no stream memory operations), STRATA_ERR_CUDA. */
+int strata_set_load_quota(strata_pool_t p, int32_t max_ctas, strata_stream_t stream);
+
 /* Consumer-side wait: make stream `consumer` wait until layer `layer` of operation
  * `ticket` (0 = latest) is complete — cudaStreamWaitEvent on the layer's event.  Errors as
  * strata_layer_event, plus STRATA_ERR_CUDA. */

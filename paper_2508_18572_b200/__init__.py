@@ -29,7 +29,7 @@ from ._lib import (STRATA_D2H, STRATA_ENGINE_DEFAULT, STRATA_ENGINE_LDG, STRATA_
 
 __all__ = [
     "strata_register_host_pool", "strata_unregister_host_pool", "strata_host_pool_ptr", "strata_load",
-    "strata_offload", "strata_layer_event", "strata_wait_layer", "strata_layer_elapsed_ms",
+    "strata_offload", "strata_layer_event", "strata_wait_layer", "strata_layer_elapsed_ms", "strata_set_load_quota",
     "strata_baseline_memcpy_pages", "strata_baseline_contiguous", "strata_test_ring_geometry",
     "strata_version", "strata_get_counters", "HostPool", "Requests", "StrataError",
 ]
@@ -87,6 +87,11 @@ def strata_layer_event(pool: int, ticket: int, layer: int) -> int:
     check(_lib.lib().strata_layer_event(ctypes.c_void_p(pool), ticket, layer, ctypes.byref(ev)),
           "strata_layer_event")
     return int(ev.value)
+
+
+def strata_set_load_quota(pool: int, max_ctas: int, stream=None) -> None:
+    check(_lib.lib().strata_set_load_quota(ctypes.c_void_p(pool), max_ctas, ctypes.c_void_p(_stream_handle(stream))),
+          "strata_set_load_quota")
 
 
 def strata_wait_layer(pool: int, ticket: int, layer: int, consumer=None) -> None:
@@ -278,6 +283,9 @@ class HostPool:
 
     def layer_event(self, ticket: int, layer: int) -> int:
         return strata_layer_event(self.handle, ticket, layer)
+
+    def set_load_quota(self, max_ctas: int, stream=None) -> None:
+        strata_set_load_quota(self.handle, max_ctas, stream)
 
     def wait_layer(self, ticket: int, layer: int, consumer=None) -> None:
         strata_wait_layer(self.handle, ticket, layer, consumer)

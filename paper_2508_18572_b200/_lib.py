@@ -93,6 +93,7 @@ _lib = None
 _SIGS = {
     "strata_get_counters": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Counters)]),
     "strata_wait_layer": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p]),
+    "strata_set_load_quota": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]),
     "strata_layer_elapsed_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32,
                                                ctypes.POINTER(ctypes.c_float)]),
     "strata_register_host_pool": (ctypes.c_int, [ctypes.POINTER(PoolDesc), ctypes.POINTER(ctypes.c_void_p)]),

@@ -521,6 +521,17 @@ int strata_wait_layer(strata_pool_t p, uint64_t ticket, int32_t layer, strata_st
   return e == cudaSuccess ? STRATA_OK : cuda_fail(e, "cudaStreamWaitEvent");
 }
 
+int strata_set_load_quota(strata_pool_t p, int32_t max_ctas, strata_stream_t stream) {
+  if (!p) return fail(STRATA_ERR_INVALID_ARG, "pool is NULL");
+  if (max_ctas < 0) return fail(STRATA_ERR_INVALID_ARG, "max_ctas = %d < 0", max_ctas);
+  strata::DeviceGuard dg(p->d.device);
+  if (!strata::ensure_fused(p)) return fail(STRATA_ERR_UNSUPPORTED, "one-launch operations are unavailable on this device");
+  const cudaError_t e = strata::set_load_quota(p, max_ctas, reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorStreamCaptureUnsupported)
+    return fail(STRATA_ERR_UNSUPPORTED, "the first strata_set_load_quota of a pool must run outside stream capture");
+  return e == cudaSuccess ? STRATA_OK : cuda_fail(e, "cuStreamWriteValue32");
+}
+
 int strata_layer_elapsed_ms(strata_pool_t p, uint64_t ticket, int32_t layer, float* ms) {
   if (!ms) return fail(STRATA_ERR_INVALID_ARG, "ms is NULL");
   int slot = 0;

@@ -92,6 +92,9 @@ struct FusedParams {
   uint32_t* flags;              // [L] completion flags of this op slot
   uint32_t* loads_active;       // load: the device-wide running-load counter ring offloads pace beside
                                 // (ring_loads_active()); NULL for offloads
+  uint32_t* next;               // [L] row-group counters of this op slot (dynamic assignment, quota path)
+  const int32_t* quota;         // load: the pool's quota word (strata_set_load_quota), or NULL: static
+                                // group assignment (ldg_fused_kernel); else ldg_quota_kernel
   char* kb[kMaxFusedLayers];    // per-layer K / V bases
   char* vb[kMaxFusedLayers];
 };
@@ -227,7 +230,8 @@ struct strata_pool {
   int64_t slot_cap = 0;
   // fused LDG operations (lazy): per op slot, L arrival counters + L layer flags (device), and a side
   // stream that turns each flag into the layer's event (cuStreamWaitValue32 + cudaEventRecord)
-  uint32_t* fused_sync = nullptr;     // [kEventRing][2][L]
+  uint32_t* fused_sync = nullptr;     // [kEventRing][3][L]: arrival counters, layer flags, group counters
+  int32_t* quota = nullptr;           // decode-aware load quota word (strata_set_load_quota), or NULL
   cudaStream_t side[strata::kEventRing] = {};
   int fused_state = 0;                // 0 untried, 1 ready, -1 unavailable (stream memory ops missing)
 };
@@ -334,6 +338,7 @@ int transfer_dma(strata_pool* p, const strata_xfer* x, const Plan& plan, XferPar
                  int dir, int slot_ev);                                                       // dma.cpp
 void free_dma(strata_pool* p);
 void free_fused(strata_pool* p);
+cudaError_t set_load_quota(strata_pool* p, int32_t max_ctas, cudaStream_t s);   // transfer.cpp
 bool ensure_fused(strata_pool* p);   // fused-LDG resources; false: unavailable (per-layer path) transfer.cpp
 // Consumer-side wait on a fused operation's layer flag (stream memory op), transfer.cpp.
 cudaError_t wait_fused_layer(strata_pool* p, int slot, int32_t layer, cudaStream_t consumer);                                                              // transfer.cpp                                                                // dma.cpp

@@ -105,6 +105,53 @@ __device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x,
 // ---------------------------------------------------------------------------------------------
 // LDG engine.  DIR 0: host -> device, DIR 1: device -> host.  CONTIG: device rows head-contiguous
 // (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
+// One row group (rows row0 .. row0 + RG - 1 of this layer's K|V rows) by one warp: lane t holds the
+// fetched indices of row t (`cur`); its host and device addresses go to the other lanes by shuffle.
+template <int U, bool CONTIG, bool HCONTIG, int DIR>
+__device__ __forceinline__ void ldg_group(const XferParams& p, const RowIdx& cur, char* kbase, char* vbase,
+                                          int64_t layer_off, int64_t row0, int64_t nrows, int lane) {
+  const int nr = static_cast<int>(min(static_cast<int64_t>(p.rows_per_group), nrows - row0));
+  char* hp = nullptr;
+  char* dp = nullptr;
+  if (cur.kv >= 0) row_finish(p, cur, kbase, vbase, layer_off, hp, dp);   // by lane, broadcast below
+  const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
+  const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
+  const int nvec = nr * p.vpt;
+  for (int base = 0; base < nvec; base += 32 * U) {
+    int4 v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int idx = base + j * 32 + lane;
+      const int rl = vec_row(p, idx);
+      const int w = idx - rl * p.vpt;
+      const uint64_t s = __shfl_sync(kFull, my_src, rl & 31);
+      if (idx < nvec) {
+        const uint64_t a = DIR == 0 ? row_vec<HCONTIG>(s, w, p, p.host_head_stride)
+                                    : row_vec<CONTIG>(s, w, p, p.head_stride);
+        v[j] = ld_stream(reinterpret_cast<const void*>(a));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int idx = base + j * 32 + lane;
+      const int rl = vec_row(p, idx);
+      const int w = idx - rl * p.vpt;
+      const uint64_t d = __shfl_sync(kFull, my_dst, rl & 31);
+      if (idx < nvec) {
+        const uint64_t a = DIR == 0 ? row_vec<CONTIG>(d, w, p, p.head_stride)
+                                    : row_vec<HCONTIG>(d, w, p, p.host_head_stride);
+        st_vec(reinterpret_cast<void*>(a), v[j]);
+      }
+    }
+  }
+}
+
+// Indices of row `lane` of group gi (row_none past the end).
+__device__ __forceinline__ RowIdx ldg_fetch(const XferParams& p, int64_t gi, int64_t ngroups, int64_t nrows, int lane) {
+  const int64_t row = gi * p.rows_per_group + lane;
+  return (gi < ngroups && lane < p.rows_per_group && row < nrows) ? row_fetch(p, row) : row_none();
+}
+
 // One layer of the LDG engine for this warp: groups warp, warp + nwarps, ...  `nx` holds the
 // already-fetched indices of the warp's first group (identical for every layer).
 template <int U, bool CONTIG, bool HCONTIG, int DIR>
@@ -115,48 +162,10 @@ __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char
   const int64_t ngroups = (nrows + RG - 1) / RG;
   // lane t fetches row t of the group; the next group's fetch is issued before this group's data
   // loads so its latency hides under them
-  auto fetch = [&](int64_t gi) {
-    const int64_t row = gi * RG + lane;
-    return (gi < ngroups && lane < RG && row < nrows) ? row_fetch(p, row) : row_none();
-  };
   for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
-    const int64_t row0 = gi * RG;
-    const int nr = static_cast<int>(min(static_cast<int64_t>(RG), nrows - row0));
     const RowIdx cur = nx;
-    nx = fetch(gi + nwarps);
-    char* hp = nullptr;
-    char* dp = nullptr;
-    if (cur.kv >= 0) row_finish(p, cur, kbase, vbase, layer_off, hp, dp);   // by lane, broadcast below
-    const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
-    const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
-    const int nvec = nr * p.vpt;
-    for (int base = 0; base < nvec; base += 32 * U) {
-      int4 v[U];
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int idx = base + j * 32 + lane;
-        const int rl = vec_row(p, idx);
-        const int w = idx - rl * p.vpt;
-        const uint64_t s = __shfl_sync(kFull, my_src, rl & 31);
-        if (idx < nvec) {
-          const uint64_t a = DIR == 0 ? row_vec<HCONTIG>(s, w, p, p.host_head_stride)
-                                      : row_vec<CONTIG>(s, w, p, p.head_stride);
-          v[j] = ld_stream(reinterpret_cast<const void*>(a));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int idx = base + j * 32 + lane;
-        const int rl = vec_row(p, idx);
-        const int w = idx - rl * p.vpt;
-        const uint64_t d = __shfl_sync(kFull, my_dst, rl & 31);
-        if (idx < nvec) {
-          const uint64_t a = DIR == 0 ? row_vec<CONTIG>(d, w, p, p.head_stride)
-                                      : row_vec<HCONTIG>(d, w, p, p.host_head_stride);
-          st_vec(reinterpret_cast<void*>(a), v[j]);
-        }
-      }
-    }
+    nx = ldg_fetch(p, gi + nwarps, ngroups, nrows, lane);
+    ldg_group<U, CONTIG, HCONTIG, DIR>(p, cur, kbase, vbase, layer_off, gi * RG, nrows, lane);
   }
 }
 
@@ -208,6 +217,80 @@ __global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_fused_kernel(const
     }
   }
   if (DIR == 0 && fp.loads_active) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicSub(fp.loads_active, 1u);
+  }
+}
+
+// Decode-aware quota (NEXT-1, strata_set_load_quota): the fused LDG load with DYNAMIC row-group
+// assignment.  Warps take the groups of layer l from next[l] (one atomicAdd per group, taken one
+// group ahead so its index fetch hides under the current group's host loads).  While the pool's
+// quota word q is > 0, CTAs with blockIdx.x >= q take no new group: their warps wait — no host reads
+// in flight from their SMs, the lever that lowers co-running decode's slowdown —
+// until the cap is lifted or every group of the layer is taken; the other CTAs move those rows.
+// Layer completion counts warps as in ldg_fused_kernel; the last arriver also resets next[l].
+__device__ __forceinline__ int32_t ld_relaxed_sys(const int32_t* a) {
+  int32_t v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int64_t quota_grab(uint32_t* next, const int32_t* quota, int64_t ngroups, int lane) {
+  uint32_t g = 0;
+  if (lane == 0) {
+    for (;;) {
+      const int32_t q = ld_relaxed_sys(quota);
+      if (q <= 0 || static_cast<int32_t>(blockIdx.x) < q) {
+        g = atomicAdd(next, 1u);
+        break;
+      }
+      if (static_cast<int64_t>(ld_relaxed_gpu(next)) >= ngroups) {   // nothing left to take this layer
+        g = static_cast<uint32_t>(ngroups);
+        break;
+      }
+      __nanosleep(2000);
+    }
+  }
+  return static_cast<int64_t>(__shfl_sync(kFull, g, 0));
+}
+
+template <int U, bool CONTIG, bool HCONTIG>
+__global__ void __launch_bounds__(U >= 8 ? 512 : 1024, 1) ldg_quota_kernel(const __grid_constant__ FusedParams fp) {
+  const XferParams& p = fp.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = static_cast<int64_t>(p.nkv) * p.ntok;
+  const int RG = p.rows_per_group;
+  const int64_t ngroups = (nrows + RG - 1) / RG;
+  const int64_t layer_step = static_cast<int64_t>(p.nkv) * p.kv_off;
+  const int total_warps = fp.total_warps;
+  if (fp.loads_active && threadIdx.x == 0) atomicAdd(fp.loads_active, 1u);   // ring offloads yield
+  for (int l = fp.l0; l < fp.l1; ++l) {
+    int64_t gi = quota_grab(fp.next + l, fp.quota, ngroups, lane);
+    RowIdx nx = ldg_fetch(p, gi, ngroups, nrows, lane);
+    while (gi < ngroups) {
+      const int64_t gn = quota_grab(fp.next + l, fp.quota, ngroups, lane);
+      const RowIdx cur = nx;
+      nx = ldg_fetch(p, gn, ngroups, nrows, lane);
+      ldg_group<U, CONTIG, HCONTIG, 0>(p, cur, fp.kb[l], fp.vb[l], int64_t(l) * layer_step, gi * RG, nrows, lane);
+      gi = gn;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      layer_fence<0>();
+      const uint32_t prev = atomicAdd(fp.counters + l, 1u);
+      if (prev == static_cast<uint32_t>(total_warps - 1)) {
+        fp.counters[l] = 0;
+        fp.next[l] = 0;   // every warp has taken its last group of layer l
+        layer_fence<0>();
+        st_release<0>(fp.flags + l, fp.epoch);
+      }
+    }
+  }
+  if (fp.loads_active) {
     __syncthreads();
     if (threadIdx.x == 0) atomicSub(fp.loads_active, 1u);
   }
@@ -457,6 +540,12 @@ cudaError_t ldg_launch(const XferParams& p, bool contig, bool hcontig, int ctas,
 
 template <int U, int DIR>
 cudaError_t ldg_fused_launch(const FusedParams& p, bool contig, bool hcontig, int ctas, int threads, cudaStream_t s) {
+  if (DIR == 0 && p.quota) {
+    if (contig && hcontig) return launch_k(ldg_quota_kernel<U, true, true>, ctas, threads, 0, s, p);
+    else if (contig) return launch_k(ldg_quota_kernel<U, true, false>, ctas, threads, 0, s, p);
+    else if (hcontig) return launch_k(ldg_quota_kernel<U, false, true>, ctas, threads, 0, s, p);
+    else return launch_k(ldg_quota_kernel<U, false, false>, ctas, threads, 0, s, p);
+  }
   if (contig && hcontig) return launch_k(ldg_fused_kernel<U, true, true, DIR>, ctas, threads, 0, s, p);
   else if (contig) return launch_k(ldg_fused_kernel<U, true, false, DIR>, ctas, threads, 0, s, p);
   else if (hcontig) return launch_k(ldg_fused_kernel<U, false, true, DIR>, ctas, threads, 0, s, p);

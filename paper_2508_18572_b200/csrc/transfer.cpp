@@ -22,6 +22,7 @@ namespace {
 
 using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 WaitValue32Fn g_wait_value32 = nullptr;
+WaitValue32Fn g_write_value32 = nullptr;   // cuStreamWriteValue32 has the same signature
 
 // STRATA_LDG_FUSED: "0" keeps the one-launch-per-layer LDG path (A/B and fallback testing);
 // "force" fuses 1-CTA grids too (profiling); default: fused from 2 CTAs.
@@ -35,7 +36,7 @@ int fused_mode() {
   return mode;
 }
 
-// Lazily: per op slot 2*L device words (arrival counters, layer flags) and a side stream; the
+// Lazily: per op slot 3*L device words (arrival counters, layer flags, row-group counters) and a side stream; the
 // driver's stream memory operation cuStreamWaitValue32 through the runtime's entry-point query,
 // probed once on a zero flag.  Unavailable -> the per-layer path is used.
 }  // namespace
@@ -53,7 +54,7 @@ bool ensure_fused(strata_pool* p) {
     }
     g_wait_value32 = reinterpret_cast<WaitValue32Fn>(fn);
   }
-  const size_t words = size_t(kEventRing) * 2 * p->d.num_layers;
+  const size_t words = size_t(kEventRing) * 3 * p->d.num_layers;
   if (cudaMalloc(&p->fused_sync, words * sizeof(uint32_t)) != cudaSuccess ||
       cudaMemset(p->fused_sync, 0, words * sizeof(uint32_t)) != cudaSuccess) {
     cudaGetLastError();
@@ -76,7 +77,7 @@ bool ensure_fused(strata_pool* p) {
 
 cudaError_t wait_fused_layer(strata_pool* p, int slot, int32_t layer, cudaStream_t consumer) {
   const int L = p->d.num_layers;
-  uint32_t* flag = p->fused_sync + size_t(slot) * 2 * L + L + layer;
+  uint32_t* flag = p->fused_sync + size_t(slot) * 3 * L + L + layer;
   const uint32_t epoch = static_cast<uint32_t>(p->ops[slot].ticket);
   return g_wait_value32(reinterpret_cast<CUstream>(consumer), reinterpret_cast<CUdeviceptr>(flag), epoch,
                         CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
@@ -92,6 +93,33 @@ void free_fused(strata_pool* p) {
   if (p->fused_sync) cudaFree(p->fused_sync);
   p->fused_sync = nullptr;
   p->fused_state = 0;
+  if (p->quota) cudaFree(p->quota);
+  p->quota = nullptr;
+}
+
+// Decode-aware quota (NEXT-1): the pool's quota word, allocated on first use (outside any capture),
+// then written in stream order by the driver's cuStreamWriteValue32.
+cudaError_t set_load_quota(strata_pool* p, int32_t max_ctas, cudaStream_t s) {
+  if (!g_write_value32) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return cudaErrorNotSupported;
+    }
+    g_write_value32 = reinterpret_cast<WaitValue32Fn>(fn);
+  }
+  cudaError_t e;
+  if (!p->quota) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if ((e = cudaStreamIsCapturing(s, &cs))) return e;
+    if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+    if ((e = cudaMalloc(&p->quota, sizeof(int32_t)))) return e;
+    if ((e = cudaMemset(p->quota, 0, sizeof(int32_t)))) return e;
+  }
+  return g_write_value32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(p->quota),
+                         static_cast<cuuint32_t>(max_ctas), 0) == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
 }
 
 int check_xfer(const strata_pool* p, const strata_xfer* x, Plan& plan) {
@@ -614,7 +642,7 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
   // memory operations are not captured here); layer events come from the device flags.
   const bool can_fuse = plan.batches.size() == 1 && x->layer_end - x->layer_begin > 1 && L <= kMaxFusedLayers &&
                         fused_mode() && cap == cudaStreamCaptureStatusNone && ensure_fused(p);
-  uint32_t* counters = p->fused_sync + size_t(slot) * 2 * L;
+  uint32_t* counters = p->fused_sync + size_t(slot) * 3 * L;
   if (engine == STRATA_ENGINE_TMA) {
     if (can_fuse) {
       if (!ring_batch(p, x, plan, plan.batches[0], rp)) return op_fail(cudaErrorInvalidValue, "ring piece count");
@@ -685,6 +713,8 @@ int transfer(strata_pool_t p, const strata_xfer* x, cudaStream_t s, uint64_t* ti
     fp.counters = counters;
     fp.flags = counters + L;
     fp.loads_active = dir == 0 ? p->loads_active : nullptr;
+    fp.next = counters + 2 * L;
+    fp.quota = dir == 0 ? p->quota : nullptr;   // set once the caller has used strata_set_load_quota
     for (int l = 0; l < L; ++l) {
       fp.kb[l] = static_cast<char*>(p->k[l]);
       fp.vb[l] = static_cast<char*>(p->v[l]);

@@ -199,6 +199,10 @@ def main():
     ap.add_argument("--tag", default="")
     ap.add_argument("--proxies", default="prefill,decode", help="prefill, decode, decode1 (one-kernel decode), decodeN (N kernels), attn (FlashInfer decode attention), decode_step (a whole Llama-8B decode step)")
     ap.add_argument("--offload", type=int, default=0, help="1: co-run offloads (write-back) instead of loads")
+    ap.add_argument("--quota-bracket", type=int, default=0,
+                    help="N > 0: also run every proxy bracketed by strata_set_load_quota(N) / (0) on its own "
+                         "stream (decode-aware quota: while the proxy runs, running LDG loads take new rows "
+                         "on N CTAs only); reported as '<proxy>@qN'")
     args = ap.parse_args()
 
     g = kvgen.geometry("llama8b_32k", P=args.P, **({"L": args.layers} if args.layers else {}))
@@ -218,6 +222,18 @@ def main():
     # decodeN: the same 8 GiB HBM read split into N reduction kernels (per-kernel-boundary cost)
     proxies = {name: (makers[name]() if name in makers else make_decode_split(int(name[len("decode"):])))
                for name in args.proxies.split(",")}
+    if args.quota_bracket:
+        pool.set_load_quota(0, stream=comp)   # loads launched from here on take rows dynamically
+        torch.cuda.synchronize()
+        qn = args.quota_bracket
+
+        def bracket(fn):
+            def run():
+                pool.set_load_quota(qn, stream=comp)
+                fn()
+                pool.set_load_quota(0, stream=comp)
+            return run
+        proxies.update({f"{name}@q{qn}": bracket(fn) for name, fn in list(proxies.items())})
     if args.graph:
         graphs = {}
         for name, fn in proxies.items():
