@@ -241,7 +241,9 @@ def interference(torch, pool, reqs, io, bytes_load, link):
     10 timed repetitions each (tests/test_gpu_interference.py runs the full 3-round protocol):
     prefill = bf16 GEMMs of a Llama-8B layer for 2 x 4K tokens; decode = an 8 GiB HBM read of 16 x 4K
     tokens of KV for 32 layers as 32 kernels; decode_long = the same read as 4 kernels; attn = the same
-    KV as the paper's decode pass run by a real kernel (FlashInfer paged decode attention, 32 layers)."""
+    KV as the paper's decode pass run by a real kernel (FlashInfer paged decode attention, 32 layers);
+    decode_step = a whole Llama-8B decode step around it; *_quota = the same bracketed by
+    strata_set_load_quota(1) / (0) (the decode-aware quota)."""
     lo, hi = torch.cuda.Stream.priority_range()
     comp = torch.cuda.Stream(priority=lo)
     M = 8192
@@ -271,6 +273,34 @@ def interference(torch, pool, reqs, io, bytes_load, link):
         qd = torch.randn(16, 32, 128, dtype=torch.bfloat16, device="cuda", generator=gen)
         od = torch.empty_like(qd)
         proxies["attn"] = lambda: [wr.run(qd, c, out=od) for c in caches]
+        # a whole Llama-8B decode step at that batch (~290 kernels): norms, QKV / O / gate-up / down
+        # GEMMs (random bf16 weights) around the same attention kernel
+        Hd = 4096
+        mk = lambda *sh: torch.randn(*sh, dtype=torch.bfloat16, device="cuda", generator=gen) * 0.02  # noqa: E731
+        wts = [(mk(Hd, 6144), mk(Hd, Hd), mk(Hd, 2 * 14336), mk(14336, Hd), mk(Hd), mk(Hd)) for _ in caches]
+        x0 = torch.randn(16, Hd, dtype=torch.bfloat16, device="cuda", generator=gen)
+
+        def decode_step():
+            F = torch.nn.functional
+            h = x0
+            for (wqkv, wo, wgu, wd, n1, n2), c in zip(wts, caches):
+                qkv = F.rms_norm(h, (Hd,), n1) @ wqkv
+                wr.run(qkv[:, :Hd].reshape(16, 32, 128), c, out=od)
+                h = h + od.reshape(16, Hd) @ wo
+                gu = F.rms_norm(h, (Hd,), n2) @ wgu
+                h = h + (F.silu(gu[:, :14336]) * gu[:, 14336:]) @ wd
+        proxies["decode_step"] = decode_step
+        # the decode-aware quota (strata_set_load_quota) bracketing the decode-side co-runners
+        pool.set_load_quota(0, stream=comp)   # loads launched from here on honour the cap
+
+        def bracket(fn):
+            def run():
+                pool.set_load_quota(1, stream=comp)
+                fn()
+                pool.set_load_quota(0, stream=comp)
+            return run
+        proxies["attn_quota"] = bracket(proxies["attn"])
+        proxies["decode_step_quota"] = bracket(decode_step)
     except Exception as ex:   # FlashInfer missing or failing on this box: the other proxies still run
         attn_note = f"attn proxy unavailable: {type(ex).__name__}: {str(ex)[:120]}"
 
@@ -305,6 +335,7 @@ def interference(torch, pool, reqs, io, bytes_load, link):
         rates.append(n_loads * bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
         out[name] = round(co / alone - 1, 4)
     out["load_gbs_beside"] = round(statistics.median(rates), 3)
+    out["load_gbs_beside_each"] = {name: round(r, 3) for name, r in zip(proxies, rates)}
     if attn_note:
         out["attn_note"] = attn_note
     out["paper_budget"] = {"prefill": 0.05, "decode": 0.10, "source": "PAPER.md:262 (H200, ~50 GB/s)"}

@@ -107,6 +107,7 @@ __device__ __forceinline__ void row_finish(const XferParams& p, const RowIdx& x,
 // (head_stride == D*e), so a device row is tok_bytes contiguous like the host row.
 // One row group (rows row0 .. row0 + RG - 1 of this layer's K|V rows) by one warp: lane t holds the
 // fetched indices of row t (`cur`); its host and device addresses go to the other lanes by shuffle.
+// (ldg_quota_kernel's body; ldg_layer keeps its own inline copy.)
 template <int U, bool CONTIG, bool HCONTIG, int DIR>
 __device__ __forceinline__ void ldg_group(const XferParams& p, const RowIdx& cur, char* kbase, char* vbase,
                                           int64_t layer_off, int64_t row0, int64_t nrows, int lane) {
@@ -161,11 +162,50 @@ __device__ __forceinline__ void ldg_layer(const XferParams& p, char* kbase, char
   const int RG = p.rows_per_group;
   const int64_t ngroups = (nrows + RG - 1) / RG;
   // lane t fetches row t of the group; the next group's fetch is issued before this group's data
-  // loads so its latency hides under them
+  // loads so its latency hides under them.  (The body is ldg_group's, kept inline here: the measured
+  // default kernel — folding it into the shared helper cost 1.6 % of its rate, profiles/r02/final5.)
+  auto fetch = [&](int64_t gi) {
+    const int64_t row = gi * RG + lane;
+    return (gi < ngroups && lane < RG && row < nrows) ? row_fetch(p, row) : row_none();
+  };
   for (int64_t gi = warp; gi < ngroups; gi += nwarps) {
+    const int64_t row0 = gi * RG;
+    const int nr = static_cast<int>(min(static_cast<int64_t>(RG), nrows - row0));
     const RowIdx cur = nx;
-    nx = ldg_fetch(p, gi + nwarps, ngroups, nrows, lane);
-    ldg_group<U, CONTIG, HCONTIG, DIR>(p, cur, kbase, vbase, layer_off, gi * RG, nrows, lane);
+    nx = fetch(gi + nwarps);
+    char* hp = nullptr;
+    char* dp = nullptr;
+    if (cur.kv >= 0) row_finish(p, cur, kbase, vbase, layer_off, hp, dp);   // by lane, broadcast below
+    const uint64_t my_src = reinterpret_cast<uint64_t>(DIR == 0 ? hp : dp);
+    const uint64_t my_dst = reinterpret_cast<uint64_t>(DIR == 0 ? dp : hp);
+    const int nvec = nr * p.vpt;
+    for (int base = 0; base < nvec; base += 32 * U) {
+      int4 v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int idx = base + j * 32 + lane;
+        const int rl = vec_row(p, idx);
+        const int w = idx - rl * p.vpt;
+        const uint64_t s = __shfl_sync(kFull, my_src, rl & 31);
+        if (idx < nvec) {
+          const uint64_t a = DIR == 0 ? row_vec<HCONTIG>(s, w, p, p.host_head_stride)
+                                      : row_vec<CONTIG>(s, w, p, p.head_stride);
+          v[j] = ld_stream(reinterpret_cast<const void*>(a));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int idx = base + j * 32 + lane;
+        const int rl = vec_row(p, idx);
+        const int w = idx - rl * p.vpt;
+        const uint64_t d = __shfl_sync(kFull, my_dst, rl & 31);
+        if (idx < nvec) {
+          const uint64_t a = DIR == 0 ? row_vec<CONTIG>(d, w, p, p.head_stride)
+                                      : row_vec<HCONTIG>(d, w, p, p.host_head_stride);
+          st_vec(reinterpret_cast<void*>(a), v[j]);
+        }
+      }
+    }
   }
 }
 

@@ -73,17 +73,21 @@ def test_layerwise_prefill_over_streaming_pages_matches_oracle_kv(engine, P):
         ref = [wrapper.run(qs, (view(kr[l]), view(vr[l]))) for l in range(g.L)]
         torch.cuda.synchronize()
 
+        # outputs allocated up front: an allocation inside the consumer loop can make the caching
+        # allocator release blocks (a device-wide synchronisation that would wait for the whole load)
+        outs = [torch.empty_like(r) for r in ref]
         io, comp = torch.cuda.Stream(), torch.cuda.Stream()
+        torch.cuda.synchronize()
         with torch.cuda.stream(io):
             torch.cuda._sleep(100_000_000)   # ~50 ms: every consumer wait is enqueued before the load starts
         t = pool.load(reqs, stream=io, engine=engine)
         load_done = torch.cuda.Event(enable_timing=True)
         load_done.record(io)
-        outs, first_done = [], torch.cuda.Event(enable_timing=True)
+        first_done = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(comp):
             for l in range(g.L):
                 pool.wait_layer(t, l, comp)
-                outs.append(wrapper.run(qs, (view(k[l]), view(v[l]))))
+                wrapper.run(qs, (view(k[l]), view(v[l])), out=outs[l])
                 if l == 0:
                     first_done.record(comp)
         torch.cuda.synchronize()
