@@ -139,22 +139,26 @@ def test_bubble_fill_keeps_the_link_busy():
         pool.load(reqs, stream=io)
         gr.replay()
         torch.cuda.synchronize()
-        a, b, d0, d1 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-        a.record(io)
-        pool.load(reqs, stream=io)             # one operation: one persistent kernel for all layers
-        b.record(io)
-        with torch.cuda.stream(dec):
-            d0.record(dec)
-            steps = 0
-            while not io.query() and steps < 2000:   # decode steps keep coming while the load runs
-                gr.replay()
-                steps += 1
-                if steps % 4 == 0:
-                    dec.synchronize()                   # a shallow queue, as a serving loop keeps
-            d1.record(dec)
-        torch.cuda.synchronize()
-        gbs = bytes_load / (a.elapsed_time(b) / 1e3) / 1e9
-        assert steps > 0 and d0.elapsed_time(b) > 0, "no decode step ran beside the load"
+        rates = []
+        for _ in range(3):                     # median of three loads (one can meet a slow stretch)
+            a, b, d0, d1 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            a.record(io)
+            pool.load(reqs, stream=io)             # one operation: one persistent kernel for all layers
+            b.record(io)
+            with torch.cuda.stream(dec):
+                d0.record(dec)
+                steps = 0
+                while not io.query() and steps < 2000:   # decode steps keep coming while the load runs
+                    gr.replay()
+                    steps += 1
+                    if steps % 4 == 0:
+                        dec.synchronize()                   # a shallow queue, as a serving loop keeps
+                d1.record(dec)
+            torch.cuda.synchronize()
+            assert steps > 0 and d0.elapsed_time(b) > 0, "no decode step ran beside the load"
+            rates.append(bytes_load / (a.elapsed_time(b) / 1e3) / 1e9)
+        gbs = statistics.median(rates)
+        print(f"load beside decode {[round(r, 1) for r in rates]} GB/s, link {link:.1f}")
         assert gbs >= 0.85 * link, f"load {gbs:.1f} GB/s beside decode < 85 % of the {link:.1f} GB/s link"
     finally:
         pool.close()
