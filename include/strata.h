@@ -259,9 +259,9 @@ int strata_layer_event(strata_pool_t p, uint64_t ticket, int32_t layer, strata_e
  * 0..q-1 move the rest, so every result stays bit-exact and every layer event still fires.  Typical
  * use: strata_set_load_quota(pool, 1, decode_stream) before a decode step, (pool, 0, decode_stream)
  * after it.  Loads launched before the first call, ring / per-layer launches and offloads ignore
- * it.  The first call allocates the word and must not run under stream capture
- * (STRATA_ERR_UNSUPPORTED); later calls may be captured.  Errors: STRATA_ERR_INVALID_ARG
- * (max_ctas < 0), STRATA_ERR_UNSUPPORTED (no stream memory operations), STRATA_ERR_CUDA. */
+ * it.  The word is library-owned device memory, zeroed at registration; calls may be captured
+ * into CUDA graphs.  Errors: STRATA_ERR_INVALID_ARG (max_ctas < 0), STRATA_ERR_UNSUPPORTED (no
+ * stream memory operations), STRATA_ERR_CUDA. */
 int strata_set_load_quota(strata_pool_t p, int32_t max_ctas, strata_stream_t stream);
 
 /* Consumer-side wait: make stream `consumer` wait until layer `layer` of operation

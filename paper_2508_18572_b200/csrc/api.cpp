@@ -527,8 +527,7 @@ int strata_set_load_quota(strata_pool_t p, int32_t max_ctas, strata_stream_t str
   strata::DeviceGuard dg(p->d.device);
   if (!strata::ensure_fused(p)) return fail(STRATA_ERR_UNSUPPORTED, "one-launch operations are unavailable on this device");
   const cudaError_t e = strata::set_load_quota(p, max_ctas, reinterpret_cast<cudaStream_t>(stream));
-  if (e == cudaErrorStreamCaptureUnsupported)
-    return fail(STRATA_ERR_UNSUPPORTED, "the first strata_set_load_quota of a pool must run outside stream capture");
+  if (e == cudaErrorNotSupported) return fail(STRATA_ERR_UNSUPPORTED, "cuStreamWriteValue32 is unavailable");
   return e == cudaSuccess ? STRATA_OK : cuda_fail(e, "cuStreamWriteValue32");
 }
 

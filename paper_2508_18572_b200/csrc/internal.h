@@ -231,7 +231,7 @@ struct strata_pool {
   // fused LDG operations (lazy): per op slot, L arrival counters + L layer flags (device), and a side
   // stream that turns each flag into the layer's event (cuStreamWaitValue32 + cudaEventRecord)
   uint32_t* fused_sync = nullptr;     // [kEventRing][3][L]: arrival counters, layer flags, group counters
-  int32_t* quota = nullptr;           // decode-aware load quota word (strata_set_load_quota), or NULL
+  int32_t* quota = nullptr;           // decode-aware load quota word (in fused_sync) once strata_set_load_quota ran, else NULL
   cudaStream_t side[strata::kEventRing] = {};
   int fused_state = 0;                // 0 untried, 1 ready, -1 unavailable (stream memory ops missing)
 };

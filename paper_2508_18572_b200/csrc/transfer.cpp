@@ -54,7 +54,7 @@ bool ensure_fused(strata_pool* p) {
     }
     g_wait_value32 = reinterpret_cast<WaitValue32Fn>(fn);
   }
-  const size_t words = size_t(kEventRing) * 3 * p->d.num_layers;
+  const size_t words = size_t(kEventRing) * 3 * p->d.num_layers + 1;   // + the decode-aware quota word
   if (cudaMalloc(&p->fused_sync, words * sizeof(uint32_t)) != cudaSuccess ||
       cudaMemset(p->fused_sync, 0, words * sizeof(uint32_t)) != cudaSuccess) {
     cudaGetLastError();
@@ -93,12 +93,12 @@ void free_fused(strata_pool* p) {
   if (p->fused_sync) cudaFree(p->fused_sync);
   p->fused_sync = nullptr;
   p->fused_state = 0;
-  if (p->quota) cudaFree(p->quota);
-  p->quota = nullptr;
+  p->quota = nullptr;   // a word of fused_sync
 }
 
-// Decode-aware quota (NEXT-1): the pool's quota word, allocated on first use (outside any capture),
-// then written in stream order by the driver's cuStreamWriteValue32.
+// Decode-aware quota (NEXT-1): the pool's quota word (the last word of fused_sync, zeroed with it at
+// registration), written in stream order by the driver's cuStreamWriteValue32; the first call makes
+// the pool's later one-launch LDG loads read it.
 cudaError_t set_load_quota(strata_pool* p, int32_t max_ctas, cudaStream_t s) {
   if (!g_write_value32) {
     void* fn = nullptr;
@@ -110,14 +110,7 @@ cudaError_t set_load_quota(strata_pool* p, int32_t max_ctas, cudaStream_t s) {
     }
     g_write_value32 = reinterpret_cast<WaitValue32Fn>(fn);
   }
-  cudaError_t e;
-  if (!p->quota) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if ((e = cudaStreamIsCapturing(s, &cs))) return e;
-    if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
-    if ((e = cudaMalloc(&p->quota, sizeof(int32_t)))) return e;
-    if ((e = cudaMemset(p->quota, 0, sizeof(int32_t)))) return e;
-  }
+  if (!p->quota) p->quota = reinterpret_cast<int32_t*>(p->fused_sync + size_t(kEventRing) * 3 * p->d.num_layers);
   return g_write_value32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(p->quota),
                          static_cast<cuuint32_t>(max_ctas), 0) == CUDA_SUCCESS ? cudaSuccess : cudaErrorUnknown;
 }

@@ -112,6 +112,33 @@ def test_cap_confines_the_host_reads_to_one_cta():
         c.close()
 
 
+def test_quota_writes_captured_in_a_graph():
+    """A decode step captured into a CUDA graph with its quota bracket (serving engines replay decode
+    from graphs): the writes replay with it, the load beside the replays stays exact."""
+    g, q = _case(seed=8, L=6, n=6000, P=2)
+    c = GpuCase(g, q)
+    try:
+        io, dec = torch.cuda.Stream(), torch.cuda.Stream()
+        c.pool.set_load_quota(0, stream=dec)
+        x = torch.zeros(1 << 24, dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=dec):
+            c.pool.set_load_quota(1, stream=torch.cuda.current_stream())
+            x.add_(1.0)
+            c.pool.set_load_quota(0, stream=torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        c.pool.load(c.reqs, stream=io, engine=LDG, num_ctas=4)
+        with torch.cuda.stream(dec):
+            for _ in range(20):
+                gr.replay()
+        torch.cuda.synchronize()
+        c.check_load(0, g.L)
+        assert float(x[0]) == 20.0
+    finally:
+        c.close()
+
+
 def test_quota_argument_errors():
     g, q = _case()
     c = GpuCase(g, q)
