@@ -3,7 +3,8 @@ BASELINE.json workloads at their real sizes, in the launch configuration bench.p
 engine's default SM quota), EVERY layer compared byte for byte with the CPU oracle, streamed one
 layer at a time (one layer's device buffers and its oracle image in host memory at once).
 
-Engines: the ring engine (STRATA_ENGINE_TMA, the default) and the LDG engine, both zero-copy
+Engines: the ring engine (STRATA_ENGINE_TMA; the default for offloads) and the LDG engine (the
+default for loads of >= 16 MiB of 16-byte rows), both zero-copy
 kernels reading / writing the host tier through its UVA mapping.  Loads start from a
 canary-filled pool, so "nothing else was touched" is part of every layer's comparison.  Offloads
 write into a canary-filled tier through a FRESH chunk list; each layer's blocks of the touched
