@@ -105,8 +105,8 @@ def test_bubble_fill_keeps_the_link_busy(engine, floor):
     """Bubble filling: the load is issued, then decode steps (an HBM read of 16 x 4K
     tokens of KV per layer, 32 layers, replayed from a CUDA graph as serving engines run decode) are
     queued into its stall and outlast it; the ring-engine load keeps >= 85 % of the measured
-    contiguous link beside them (measured ~50 GB/s), the default (LDG) load >= 80 % (measured
-    47.1-48.8 GB/s = 0.85-0.88: it yields more of the link to decode).  (The load goes first: a persistent I/O kernel issued behind a
+    contiguous link beside them (measured 48.1-48.3 GB/s = 0.87), the default (LDG) load >= 80 %
+    (measured 46.9-48.8 GB/s = 0.85-0.88: it yields more of the link to decode).  (The load goes first: a persistent I/O kernel issued behind a
     GPU-filling decode stream waits for SM space — DESIGN.md §6.)"""
     g = kvgen.geometry("llama8b_32k")
     q = kvgen.make_requests(kvgen.rng_for(1), [32768], g.P, g.C, g.num_pages, g.num_chunks)
